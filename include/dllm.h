@@ -1,0 +1,146 @@
+/*
+ * dllm.h — C-ABI of libdllm: dLLM-Serve's Head-Centric Sparse Attention hot
+ * path (arXiv 2512.17077) on NVIDIA B200 (sm_100a).
+ *
+ * Three calls make up one pass of the path:
+ *   dllm_refresh_attn       Refresh, Eq. 3 (§2.3) + the raw
+ *                           per-head importance of Eq. 6 (§4.5)
+ *   dllm_select_heads       local max-pool + per-head TopK (§4.5)
+ *   dllm_reuse_sparse_attn  Reuse, Eq. 4 (§2.3) over the
+ *                           per-head key subsets of §4.5
+ *
+ * Plain C: no torch or CUDA types in the signatures.  Device buffers are
+ * plain device pointers owned by the caller; host arrays are read during the
+ * call only.  The library never allocates device memory on a call path and
+ * never writes the K/V cache.
+ *
+ * Execution: compute calls enqueue kernels on `stream` (a cudaStream_t cast
+ * to void*, NULL = legacy default stream) and return without synchronising.
+ * They are CUDA-graph capturable.  Validation is all-or-nothing: on any
+ * error nothing is enqueued.  Faults inside a kernel surface at the caller's
+ * next synchronisation.
+ *
+ * Layouts (all bf16 tensors 16-byte aligned, row-major, innermost last):
+ *   q, out         [sum_b L_b, H, D]   packed varlen, request b at rows
+ *                                      cu_L[b] = sum_{b'<b} L_b'
+ *   q_blk, out_blk [sum_b blk_b, H, D] the active blocks, request order,
+ *                                      blk_b = be_b - bs_b
+ *   k_cache,       [num_pages, H_kv, P, D]  paged, head-major inside a page:
+ *   v_cache                            position p of request b is page
+ *                                      block_table[b*pages_per_req + p/P],
+ *                                      slot p%P.  Keys are post-RoPE
+ *                                      (R13).
+ *   scores (fp32)  scores[H*cu_L[b] + h*L_b + m], m in [0, L_b): the raw,
+ *                  UNSCALED max_{q in [bs,be)} Q[q,h].K[m,kv(h)] (DESIGN.md
+ *                  R1, R8); block positions are written but not used.
+ *   idx (int32)    idx[H*cu_k[b] + h*k_b + i], i in [0, k_b): selected
+ *                  sequence positions, strictly ascending per (b, h), outside
+ *                  [bs, be); cu_k[b] = sum_{b'<b} k_b'; k_b = dllm_keep_count
+ *                  (keep_ratio, L_b - blk_b).
+ * GQA: query head h reads KV head h / (H / H_kv) (R10).
+ */
+#ifndef DLLM_H_
+#define DLLM_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DLLM_API __attribute__((visibility("default")))
+#else
+#define DLLM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (0 = success) ---------------------------------------- */
+#define DLLM_OK                0
+#define DLLM_ERR_INVALID_ARG  (-1)  /* NULL pointer, r not in (0,1], w even, ... */
+#define DLLM_ERR_UNSUPPORTED  (-2)  /* head_dim / page_size / length outside the built kernels */
+#define DLLM_ERR_SHAPE        (-3)  /* H % H_kv != 0, bs/be outside [0, L], misaligned buffers */
+#define DLLM_ERR_K_RANGE      (-4)  /* k > n_ctx (only reachable through dllm_check_indices) */
+#define DLLM_ERR_CUDA         (-5)  /* a CUDA launch / attribute call failed */
+
+#define DLLM_MAX_SEQ_LEN   65536   /* L_b upper bound for refresh / reuse            */
+#define DLLM_MAX_SELECT_LEN 32768  /* L_b upper bound for dllm_select_heads (smem)   */
+#define DLLM_MAX_BLOCK     128     /* blk_b = be_b - bs_b upper bound                */
+
+/* The problem statement of one batch (a packed batch
+ * of requests with per-request sequence length and active-block position;
+ * heads / KV heads / head_dim; keep ratio r; pooling
+ * window w). */
+typedef struct dllm_problem {
+  int32_t num_requests;        /* B >= 0                                          */
+  int32_t num_heads;           /* H >= 1                                          */
+  int32_t num_kv_heads;        /* H_kv >= 1, H % H_kv == 0                        */
+  int32_t head_dim;            /* D in {16, 32, 64, 128}                          */
+  const int32_t *seq_len;      /* HOST [B]: 1 <= L_b <= DLLM_MAX_SEQ_LEN          */
+  const int32_t *blk_start;    /* HOST [B]: 0 <= bs_b                             */
+  const int32_t *blk_end;      /* HOST [B]: bs_b < be_b <= L_b, be-bs <= 128      */
+  double keep_ratio;           /* r in (0, 1]                                     */
+  int32_t pool_window;         /* w odd >= 1 (Table 3 "Kernel Size" = 3)          */
+  float softmax_scale;         /* tau; 0 -> 1/sqrt(D) (Eq. 3/4 "sqrt(d)")         */
+  int32_t page_size;           /* P: power of two in [16, 1024]                   */
+  int32_t pages_per_req;       /* row stride of block_table, >= ceil(L_b / P)     */
+  const int32_t *block_table;  /* DEVICE [B * pages_per_req] physical page ids    */
+} dllm_problem;
+
+/* k = ceil(r * n_ctx) in IEEE double, clamped to [1, n_ctx]; 0 if n_ctx == 0
+ * ("k = L*r", R5).  Returns a negative status for
+ * r not in (0, 1] or n_ctx < 0.  Host only. */
+DLLM_API int dllm_keep_count(double keep_ratio, int32_t n_ctx);
+
+/* Validates `p` (host fields only; no CUDA call) and reports the index
+ * layout: k_out (HOST [B], may be NULL) receives k_b, *total_idx (may be
+ * NULL) receives H * sum_b k_b, the int32 count `idx` must hold.  Also the
+ * size helpers: *total_rows = sum L_b, *total_blk_rows = sum blk_b (NULL ok). */
+DLLM_API int dllm_index_layout(const dllm_problem *p, int32_t *k_out, int64_t *total_idx,
+                      int64_t *total_rows, int64_t *total_blk_rows);
+
+/* Refresh (Eq. 3): out[q, h] = softmax_j(tau * Q[q,h].K[j,kv(h)]) . V[j,kv(h)]
+ * over all j in [0, L_b) (bidirectional, no mask), for every row of every
+ * request; bf16 in, fp32 accumulation and softmax statistics, P rounded to
+ * bf16 before P.V, bf16 out (R14).  If `scores` is not NULL it also
+ * writes the raw importance (see layout above).  q, k_cache, v_cache, out,
+ * scores: DEVICE. */
+DLLM_API int dllm_refresh_attn(const dllm_problem *p, const void *q, const void *k_cache,
+                      const void *v_cache, void *out, float *scores, void *stream);
+
+/* Selection (Eq. 6 + TopK): per (b, h), over the candidates
+ * C = [0, bs) ++ [be, L) (R4): S[c] = max of scores[C[c']] for
+ * |c' - c| <= w/2, c' in [0, n_ctx) (pooling on the compacted candidate axis,
+ * R2-R4); I^h = the k_b candidates with the largest S, ties to the lower c
+ * (R6), written as positions C[c] ascending (R7).  Bit-exact.  -0 == +0.
+ * Scores must be finite.  scores, idx: DEVICE. */
+DLLM_API int dllm_select_heads(const dllm_problem *p, const float *scores, int32_t *idx, void *stream);
+
+/* Reuse (Eq. 4): out_blk[q, h] = softmax_j(tau * Qb[q,h].K[j,kv(h)]) . V[j,kv(h)]
+ * over J^h = [bs, be) ++ idx(b, h), K/V read in place through the block table
+ * (no pack, no copy).  The caller has written the active block's K/V rows
+ * into the cache.  idx must satisfy the layout precondition above (checked
+ * only by dllm_check_indices).  q_blk, k_cache, v_cache, idx, out_blk: DEVICE. */
+DLLM_API int dllm_reuse_sparse_attn(const dllm_problem *p, const void *q_blk, const void *k_cache,
+                           const void *v_cache, const int32_t *idx, void *out_blk,
+                           void *stream);
+
+/* Debug: counts index-layout violations (out of [0, L), inside the block,
+ * not strictly ascending) into *d_violations (DEVICE int32, zeroed by the
+ * call).  idx, d_violations: DEVICE. */
+DLLM_API int dllm_check_indices(const dllm_problem *p, const int32_t *idx, int32_t *d_violations,
+                       void *stream);
+
+/* Static description of a status code. */
+DLLM_API const char *dllm_status_string(int status);
+
+/* Thread-local detail of the last failing call on this thread ("" if none). */
+DLLM_API const char *dllm_last_error(void);
+
+/* Library build / kernel identification string (architecture, kernels). */
+DLLM_API const char *dllm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DLLM_H_ */

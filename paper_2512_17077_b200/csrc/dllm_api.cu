@@ -1,0 +1,330 @@
+// libdllm host side: the C-ABI of include/dllm.h.
+//
+// Validates the problem synchronously (all-or-nothing: nothing is enqueued
+// on error), computes the per-request layout (k_b, offsets), packs it into
+// by-value launch plans (plan.h) of at most kMaxReqPerLaunch requests, and
+// enqueues the kernels on the caller's stream.  No device allocation, no
+// host<->device copy, no synchronisation on any call path.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdlib.h>
+#include <stddef.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/dllm.h"
+#include "plan.h"
+
+namespace dllm {
+cudaError_t launch_select(const Plan &, const float *, int32_t *, cudaStream_t);
+cudaError_t launch_check_indices(const Plan &, const int32_t *, int32_t *, cudaStream_t);
+cudaError_t launch_reuse(const Plan &, const void *, const void *, const void *, const int32_t *, void *,
+                         cudaStream_t);
+cudaError_t launch_refresh_mma(const Plan &, const void *, const void *, const void *, void *, float *,
+                               cudaStream_t);
+int refresh_mma_units(int L, int bs, int be, int H, bool with_scores);
+bool refresh_tc_supported(int D);
+int refresh_tc_units(int L, int bs, int be, int H, bool with_scores);
+cudaError_t launch_refresh_tc(const Plan &, const void *, const void *, const void *, void *, float *,
+                              cudaStream_t);
+}  // namespace dllm
+
+using namespace dllm;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int ok() {
+  g_last_error.clear();
+  return DLLM_OK;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int keep_count_impl(double r, int32_t n) {
+  if (!(r > 0.0 && r <= 1.0) || n < 0) return DLLM_ERR_INVALID_ARG;
+  if (n == 0) return 0;
+  double k = ceil(r * (double)n);   // IEEE double product, then ceil (R5)
+  if (k < 1.0) k = 1.0;
+  if (k > (double)n) k = (double)n;
+  return (int)k;
+}
+
+// Host-side validation of every field the calls read.  Fills k[] when given.
+int validate(const dllm_problem *p, std::vector<int32_t> *k) {
+  if (!p) return fail(DLLM_ERR_INVALID_ARG, "problem is NULL");
+  const int B = p->num_requests;
+  if (B < 0) return fail(DLLM_ERR_INVALID_ARG, "num_requests=%d < 0", B);
+  if (p->num_heads < 1 || p->num_kv_heads < 1)
+    return fail(DLLM_ERR_INVALID_ARG, "num_heads=%d num_kv_heads=%d must be >= 1", p->num_heads, p->num_kv_heads);
+  if (p->num_heads % p->num_kv_heads)
+    return fail(DLLM_ERR_SHAPE, "num_heads=%d is not a multiple of num_kv_heads=%d", p->num_heads,
+                p->num_kv_heads);
+  const int D = p->head_dim;
+  if (D != 16 && D != 32 && D != 64 && D != 128)
+    return fail(DLLM_ERR_UNSUPPORTED, "head_dim=%d not in {16,32,64,128}", D);
+  if (!(p->keep_ratio > 0.0 && p->keep_ratio <= 1.0))
+    return fail(DLLM_ERR_INVALID_ARG, "keep_ratio=%g not in (0,1]", p->keep_ratio);
+  if (p->pool_window < 1 || (p->pool_window & 1) == 0)
+    return fail(DLLM_ERR_INVALID_ARG, "pool_window=%d must be odd and >= 1", p->pool_window);
+  if (!(p->softmax_scale >= 0.f) || isinf(p->softmax_scale))
+    return fail(DLLM_ERR_INVALID_ARG, "softmax_scale must be finite and >= 0 (0 = 1/sqrt(D))");
+  const int P = p->page_size;
+  if (P < 16 || P > 1024 || (P & (P - 1)))
+    return fail(DLLM_ERR_UNSUPPORTED, "page_size=%d must be a power of two in [16,1024]", P);
+  if (B == 0) {
+    if (k) k->clear();
+    return DLLM_OK;
+  }
+  if (!p->seq_len || !p->blk_start || !p->blk_end)
+    return fail(DLLM_ERR_INVALID_ARG, "seq_len / blk_start / blk_end must be host arrays of length B");
+  if (!p->block_table) return fail(DLLM_ERR_INVALID_ARG, "block_table is NULL");
+  if (k) k->resize(B);
+  int64_t rows = 0;
+  for (int b = 0; b < B; ++b) {
+    const int L = p->seq_len[b], bs = p->blk_start[b], be = p->blk_end[b];
+    if (L < 1 || L > DLLM_MAX_SEQ_LEN)
+      return fail(L < 1 ? DLLM_ERR_SHAPE : DLLM_ERR_UNSUPPORTED, "request %d: seq_len=%d outside [1,%d]", b, L,
+                  DLLM_MAX_SEQ_LEN);
+    if (!(0 <= bs && bs < be && be <= L))
+      return fail(DLLM_ERR_SHAPE, "request %d: need 0 <= blk_start(%d) < blk_end(%d) <= seq_len(%d)", b, bs, be, L);
+    if (be - bs > DLLM_MAX_BLOCK)
+      return fail(DLLM_ERR_UNSUPPORTED, "request %d: block of %d rows > %d", b, be - bs, DLLM_MAX_BLOCK);
+    if ((int64_t)(L + P - 1) / P > p->pages_per_req)
+      return fail(DLLM_ERR_SHAPE, "request %d: seq_len=%d needs %d pages > pages_per_req=%d", b, L, (L + P - 1) / P,
+                  p->pages_per_req);
+    rows += L;
+    if (k) (*k)[b] = keep_count_impl(p->keep_ratio, L - (be - bs));
+  }
+  if (rows * p->num_heads * D > ((int64_t)1 << 40)) return fail(DLLM_ERR_UNSUPPORTED, "batch too large");
+  return DLLM_OK;
+}
+
+float scale_of(const dllm_problem *p) {
+  return p->softmax_scale > 0.f ? p->softmax_scale : (float)(1.0 / sqrt((double)p->head_dim));
+}
+
+// Packs requests [b0, b1) into a plan; units(b) gives each request's unit count.
+template <class UnitsFn>
+void fill_plan(Plan &pl, const dllm_problem *p, const std::vector<int32_t> &k, int b0, int b1,
+               const std::vector<int64_t> &cu_L, const std::vector<int64_t> &cu_blk,
+               const std::vector<int64_t> &cu_k, UnitsFn units) {
+  memset(&pl, 0, offsetof(Plan, r));
+  pl.nreq = b1 - b0;
+  pl.H = p->num_heads;
+  pl.H_kv = p->num_kv_heads;
+  pl.D = p->head_dim;
+  pl.page_size = p->page_size;
+  int sh = 0;
+  while ((1 << sh) < p->page_size) ++sh;
+  pl.page_shift = sh;
+  pl.pages_per_req = p->pages_per_req;
+  pl.window = p->pool_window;
+  pl.scale = scale_of(p);
+  pl.scale_log2 = (float)((double)pl.scale * 1.4426950408889634);
+  pl.block_table = p->block_table;
+  int u = 0;
+  for (int b = b0; b < b1; ++b) {
+    ReqInfo &r = pl.r[b - b0];
+    r.L = p->seq_len[b];
+    r.bs = p->blk_start[b];
+    r.be = p->blk_end[b];
+    r.q_off = (int32_t)cu_L[b];
+    r.blk_off = (int32_t)cu_blk[b];
+    r.k = k[b];
+    r.idx_off = (int64_t)p->num_heads * cu_k[b];
+    r.score_off = (int64_t)p->num_heads * cu_L[b];
+    r.unit_off = u;
+    r.bt_row = b;
+    u += units(b);
+  }
+  pl.total_units = u;
+}
+
+struct Layout {
+  std::vector<int32_t> k;
+  std::vector<int64_t> cu_L, cu_blk, cu_k;
+};
+
+int make_layout(const dllm_problem *p, Layout &lay) {
+  int st = validate(p, &lay.k);
+  if (st) return st;
+  const int B = p->num_requests;
+  lay.cu_L.assign(B + 1, 0);
+  lay.cu_blk.assign(B + 1, 0);
+  lay.cu_k.assign(B + 1, 0);
+  for (int b = 0; b < B; ++b) {
+    lay.cu_L[b + 1] = lay.cu_L[b] + p->seq_len[b];
+    lay.cu_blk[b + 1] = lay.cu_blk[b] + (p->blk_end[b] - p->blk_start[b]);
+    lay.cu_k[b + 1] = lay.cu_k[b] + lay.k[b];
+  }
+  if (lay.cu_L[B] > INT32_MAX) return fail(DLLM_ERR_UNSUPPORTED, "sum of seq_len exceeds 2^31");
+  return DLLM_OK;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+  return fail(DLLM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int refresh_impl_env() {
+  // DLLM_REFRESH_IMPL=mma forces the mma.sync kernel (A/B comparisons).
+  const char *s = getenv("DLLM_REFRESH_IMPL");
+  if (s && !strcmp(s, "mma")) return 0;
+  return 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dllm_keep_count(double keep_ratio, int32_t n_ctx) {
+  const int k = keep_count_impl(keep_ratio, n_ctx);
+  if (k < 0) return fail(k, "keep_count: keep_ratio=%g n_ctx=%d", keep_ratio, n_ctx);
+  return k;
+}
+
+int dllm_index_layout(const dllm_problem *p, int32_t *k_out, int64_t *total_idx, int64_t *total_rows,
+                      int64_t *total_blk_rows) {
+  Layout lay;
+  int st = make_layout(p, lay);
+  if (st) return st;
+  const int B = p->num_requests;
+  if (k_out)
+    for (int b = 0; b < B; ++b) k_out[b] = lay.k[b];
+  if (total_idx) *total_idx = (int64_t)p->num_heads * (B ? lay.cu_k[B] : 0);
+  if (total_rows) *total_rows = B ? lay.cu_L[B] : 0;
+  if (total_blk_rows) *total_blk_rows = B ? lay.cu_blk[B] : 0;
+  return ok();
+}
+
+int dllm_refresh_attn(const dllm_problem *p, const void *q, const void *k_cache, const void *v_cache, void *out,
+                      float *scores, void *stream) {
+  Layout lay;
+  int st = make_layout(p, lay);
+  if (st) return st;
+  const int B = p->num_requests;
+  if (B == 0) return ok();
+  if (!q || !k_cache || !v_cache || !out) return fail(DLLM_ERR_INVALID_ARG, "refresh: NULL tensor pointer");
+  if (!aligned16(q) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out))
+    return fail(DLLM_ERR_SHAPE, "refresh: bf16 tensors must be 16-byte aligned");
+  if (scores && ((uintptr_t)scores & 3u)) return fail(DLLM_ERR_SHAPE, "refresh: scores must be 4-byte aligned");
+  const bool with_scores = scores != nullptr;
+  const bool use_tc = refresh_impl_env() && refresh_tc_supported(p->head_dim);
+  cudaStream_t s = (cudaStream_t)stream;
+  static thread_local Plan pl;
+  for (int b0 = 0; b0 < B; b0 += kMaxReqPerLaunch) {
+    const int b1 = b0 + kMaxReqPerLaunch < B ? b0 + kMaxReqPerLaunch : B;
+    fill_plan(pl, p, lay.k, b0, b1, lay.cu_L, lay.cu_blk, lay.cu_k, [&](int b) {
+      return use_tc ? refresh_tc_units(p->seq_len[b], p->blk_start[b], p->blk_end[b], p->num_heads, with_scores)
+                    : refresh_mma_units(p->seq_len[b], p->blk_start[b], p->blk_end[b], p->num_heads, with_scores);
+    });
+    pl.with_scores = with_scores;
+    cudaError_t e = use_tc ? launch_refresh_tc(pl, q, k_cache, v_cache, out, scores, s)
+                           : launch_refresh_mma(pl, q, k_cache, v_cache, out, scores, s);
+    if (e != cudaSuccess) return cuda_fail(e, "refresh launch");
+  }
+  return ok();
+}
+
+int dllm_select_heads(const dllm_problem *p, const float *scores, int32_t *idx, void *stream) {
+  Layout lay;
+  int st = make_layout(p, lay);
+  if (st) return st;
+  const int B = p->num_requests;
+  if (B == 0) return ok();
+  if (!scores || !idx) return fail(DLLM_ERR_INVALID_ARG, "select: NULL pointer");
+  for (int b = 0; b < B; ++b)
+    if (p->seq_len[b] > DLLM_MAX_SELECT_LEN)
+      return fail(DLLM_ERR_UNSUPPORTED, "select: request %d seq_len=%d > %d", b, p->seq_len[b], DLLM_MAX_SELECT_LEN);
+  static thread_local Plan pl;
+  for (int b0 = 0; b0 < B; b0 += kMaxReqPerLaunch) {
+    const int b1 = b0 + kMaxReqPerLaunch < B ? b0 + kMaxReqPerLaunch : B;
+    fill_plan(pl, p, lay.k, b0, b1, lay.cu_L, lay.cu_blk, lay.cu_k, [&](int) { return p->num_heads; });
+    if (pl.total_units == 0) continue;
+    cudaError_t e = launch_select(pl, scores, idx, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "select launch");
+  }
+  return ok();
+}
+
+int dllm_reuse_sparse_attn(const dllm_problem *p, const void *q_blk, const void *k_cache, const void *v_cache,
+                           const int32_t *idx, void *out_blk, void *stream) {
+  Layout lay;
+  int st = make_layout(p, lay);
+  if (st) return st;
+  const int B = p->num_requests;
+  if (B == 0) return ok();
+  if (!q_blk || !k_cache || !v_cache || !out_blk) return fail(DLLM_ERR_INVALID_ARG, "reuse: NULL tensor pointer");
+  if (!idx && lay.cu_k[B] > 0) return fail(DLLM_ERR_INVALID_ARG, "reuse: idx is NULL");
+  if (!aligned16(q_blk) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out_blk))
+    return fail(DLLM_ERR_SHAPE, "reuse: bf16 tensors must be 16-byte aligned");
+  static thread_local Plan pl;
+  for (int b0 = 0; b0 < B; b0 += kMaxReqPerLaunch) {
+    const int b1 = b0 + kMaxReqPerLaunch < B ? b0 + kMaxReqPerLaunch : B;
+    fill_plan(pl, p, lay.k, b0, b1, lay.cu_L, lay.cu_blk, lay.cu_k, [&](int b) {
+      const int blk = p->blk_end[b] - p->blk_start[b];
+      return p->num_heads * ((blk + 31) / 32);
+    });
+    cudaError_t e = launch_reuse(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "reuse launch");
+  }
+  return ok();
+}
+
+int dllm_check_indices(const dllm_problem *p, const int32_t *idx, int32_t *d_violations, void *stream) {
+  Layout lay;
+  int st = make_layout(p, lay);
+  if (st) return st;
+  if (!d_violations) return fail(DLLM_ERR_INVALID_ARG, "check_indices: d_violations is NULL");
+  const int B = p->num_requests;
+  cudaError_t e = cudaMemsetAsync(d_violations, 0, sizeof(int32_t), (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "check_indices memset");
+  if (B == 0) return ok();
+  if (!idx && lay.cu_k[B] > 0) return fail(DLLM_ERR_INVALID_ARG, "check_indices: idx is NULL");
+  static thread_local Plan pl;
+  for (int b0 = 0; b0 < B; b0 += kMaxReqPerLaunch) {
+    const int b1 = b0 + kMaxReqPerLaunch < B ? b0 + kMaxReqPerLaunch : B;
+    fill_plan(pl, p, lay.k, b0, b1, lay.cu_L, lay.cu_blk, lay.cu_k, [&](int) { return p->num_heads; });
+    e = launch_check_indices(pl, idx, d_violations, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "check_indices launch");
+  }
+  return ok();
+}
+
+const char *dllm_status_string(int status) {
+  switch (status) {
+    case DLLM_OK: return "DLLM_OK";
+    case DLLM_ERR_INVALID_ARG: return "DLLM_ERR_INVALID_ARG";
+    case DLLM_ERR_UNSUPPORTED: return "DLLM_ERR_UNSUPPORTED";
+    case DLLM_ERR_SHAPE: return "DLLM_ERR_SHAPE";
+    case DLLM_ERR_K_RANGE: return "DLLM_ERR_K_RANGE";
+    case DLLM_ERR_CUDA: return "DLLM_ERR_CUDA";
+  }
+  return "DLLM_ERR_UNKNOWN";
+}
+
+const char *dllm_last_error(void) { return g_last_error.c_str(); }
+
+const char *dllm_version(void) {
+  return "libdllm sm_100a: refresh=tcgen05/TMEM+TMA (mma.sync fallback for D<64), select=radix-topk, "
+         "reuse=paged-gather cp.async + mma.sync";
+}
+
+}  // extern "C"

@@ -1,0 +1,52 @@
+// Launch plan shared by the host library and the kernels.
+//
+// The host validates the problem and packs per-request metadata into a plan
+// that travels BY VALUE as a __grid_constant__ kernel parameter (CUDA >= 12.1
+// allows 32 KB of parameters), so there is no hidden host->device copy and
+// the launches stay CUDA-graph capturable.  Batches larger than
+// kMaxReqPerLaunch are split into several launches.
+#pragma once
+#include <stdint.h>
+
+namespace dllm {
+
+constexpr int kMaxReqPerLaunch = 256;
+
+struct ReqInfo {
+  int32_t L;         // sequence length L_b
+  int32_t bs, be;    // active block [bs, be)
+  int32_t q_off;     // cu_L[b]: first row of the request in q / out
+  int32_t blk_off;   // cu_blk[b]: first row in q_blk / out_blk
+  int32_t k;         // k_b
+  int64_t idx_off;   // H * cu_k[b]: first element of the request in idx
+  int64_t score_off; // H * cu_L[b]: first element in scores
+  int32_t unit_off;  // prefix of work units (kernel specific) before this request
+  int32_t bt_row;    // row of the block table (request index in the caller's batch)
+};
+
+struct Plan {
+  int32_t nreq;
+  int32_t total_units;
+  int32_t H, H_kv, D;
+  int32_t page_size, page_shift, pages_per_req;
+  int32_t window;
+  int32_t with_scores;  // refresh: also emit the Eq. 6 raw importance
+  float scale_log2;  // tau * log2(e)
+  float scale;       // tau
+  const int32_t *block_table;
+  ReqInfo r[kMaxReqPerLaunch];
+};
+
+#if defined(__CUDACC__)
+// Request owning work unit u: largest b with r[b].unit_off <= u.
+__device__ __forceinline__ int plan_find(const Plan &p, int u) {
+  int lo = 0, hi = p.nreq - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (p.r[mid].unit_off <= u) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+#endif
+
+}  // namespace dllm

@@ -1,0 +1,198 @@
+// Select: local max-pool + per-head TopK (§4.5, Eq. 6).
+//
+// One CTA per (request b, query head h).  The CTA
+//   1. pools the raw scores of the n_ctx candidates C = [0,bs) ++ [be,L)
+//      on the compacted candidate axis (window half-width w/2, clipped;
+//      DESIGN.md R2-R4) straight from global memory (neighbour reads hit L1),
+//      and stores order-preserving 32-bit keys in shared memory
+//      (float -> uint, larger float -> larger key, -0 canonicalised to +0;
+//      DESIGN.md R9);
+//   2. finds the k-th largest key exactly with a 4-pass 8-bit MSB radix
+//      select (shared-memory histograms);
+//   3. compacts: every key above the threshold, plus the lowest-index
+//      (k - #above) keys equal to it (R6), written as sequence
+//      positions in ascending order (R7) with two ballot-based block scans.
+// All decisions are integer comparisons of the fp32 inputs: bit-exact.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "plan.h"
+
+namespace dllm {
+
+constexpr int kSelThreads = 512;
+constexpr int kSelWarps = kSelThreads / 32;
+
+__device__ __forceinline__ uint32_t order_key(float f) {
+  uint32_t u = __float_as_uint(f);
+  if ((u & 0x7fffffffu) == 0u) return 0x80000000u;     // +-0 -> the same key
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// Block-wide exclusive scan of one int per thread; returns the exclusive
+// prefix and writes the block total to *total.
+__device__ __forceinline__ int block_excl_scan(int v, int *warp_buf, int *total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_buf[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < kSelWarps ? warp_buf[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < kSelWarps) warp_buf[lane] = w;        // inclusive warp prefix
+  }
+  __syncthreads();
+  int base = warp ? warp_buf[warp - 1] : 0;
+  *total = warp_buf[kSelWarps - 1];
+  __syncthreads();
+  return base + x - v;
+}
+
+__global__ void __launch_bounds__(kSelThreads)
+select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__ scores,
+                    int32_t *__restrict__ idx) {
+  extern __shared__ uint32_t keys[];                  // [n_ctx]
+  __shared__ int hist[256];
+  __shared__ int warp_buf[32];
+  __shared__ uint32_t s_prefix;
+  __shared__ int s_krem;
+
+  const int unit = blockIdx.x;
+  const int b = plan_find(plan, unit);
+  const ReqInfo &R = plan.r[b];
+  const int h = unit - R.unit_off;
+  const int L = R.L, bs = R.bs, blk = R.be - R.bs;
+  const int n = L - blk;
+  const int k = R.k;
+  if (k <= 0) return;
+  const float *raw = scores + R.score_off + (int64_t)h * L;
+  int32_t *out = idx + R.idx_off + (int64_t)h * k;
+  const int half = plan.window >> 1;
+
+  // 1. pool on the compacted axis, to order keys
+  for (int c = threadIdx.x; c < n; c += kSelThreads) {
+    const int lo = max(0, c - half), hi = min(n - 1, c + half);
+    float m = -INFINITY;
+    for (int j = lo; j <= hi; ++j) {
+      const int pos = j < bs ? j : j + blk;
+      m = fmaxf(m, __ldg(raw + pos));
+    }
+    keys[c] = order_key(m);
+  }
+  if (threadIdx.x == 0) { s_prefix = 0u; s_krem = k; }
+  __syncthreads();
+
+  // 2. radix select of the k-th largest key (MSB first)
+  uint32_t prefix = 0u, mask = 0u;
+  int krem = k;
+#pragma unroll 1
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += kSelThreads) hist[i] = 0;
+    __syncthreads();
+    for (int c = threadIdx.x; c < n; c += kSelThreads) {
+      const uint32_t key = keys[c];
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 0xffu], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      // lane l owns bins [8*(31-l), 8*(31-l)+8): lane 0 holds the top bins
+      const int lane = threadIdx.x;
+      const int base = 8 * (31 - lane);
+      int cnt[8], sum = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { cnt[i] = hist[base + 7 - i]; sum += cnt[i]; }  // descending bins
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int above = incl - sum;                   // keys in higher bins than this lane's
+      const bool mine = above < krem && krem <= incl;
+      if (mine) {
+        int acc = above;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (acc + cnt[i] >= krem) {
+            const uint32_t digit = (uint32_t)(base + 7 - i);
+            s_prefix = prefix | (digit << shift);
+            s_krem = krem - acc;
+            break;
+          }
+          acc += cnt[i];
+        }
+      }
+    }
+    __syncthreads();
+    prefix = s_prefix;
+    krem = s_krem;
+    mask |= 0xffu << shift;
+    __syncthreads();
+  }
+  const uint32_t thr = prefix;   // exact key of the k-th largest
+  const int need_eq = krem;      // how many keys equal to thr are taken (lowest index first)
+
+  // 3. compaction in ascending candidate order
+  int eq_base = 0, out_base = 0;
+  for (int c0 = 0; c0 < n; c0 += kSelThreads) {
+    const int c = c0 + threadIdx.x;
+    uint32_t key = c < n ? keys[c] : 0u;
+    const int gt = (c < n) && key > thr;
+    const int eq = (c < n) && key == thr;
+    int eq_tot;
+    const int eq_rank = eq_base + block_excl_scan(eq, warp_buf, &eq_tot);
+    const int sel = gt || (eq && eq_rank < need_eq);
+    int sel_tot;
+    const int pos_out = out_base + block_excl_scan(sel, warp_buf, &sel_tot);
+    if (sel) out[pos_out] = c < bs ? c : c + blk;
+    eq_base += eq_tot;
+    out_base += sel_tot;
+  }
+}
+
+// Debug checker: counts positions out of range, inside the block, or not
+// strictly ascending.
+__global__ void check_indices_kernel(const __grid_constant__ Plan plan, const int32_t *__restrict__ idx,
+                                     int32_t *violations) {
+  const int unit = blockIdx.x;
+  const int b = plan_find(plan, unit);
+  const ReqInfo &R = plan.r[b];
+  const int h = unit - R.unit_off;
+  const int32_t *row = idx + R.idx_off + (int64_t)h * R.k;
+  int bad = 0;
+  for (int i = threadIdx.x; i < R.k; i += blockDim.x) {
+    const int p = row[i];
+    if (p < 0 || p >= R.L || (p >= R.bs && p < R.be)) ++bad;
+    if (i > 0 && row[i - 1] >= p) ++bad;
+  }
+  if (bad) atomicAdd(violations, bad);
+}
+
+cudaError_t launch_select(const Plan &plan, const float *scores, int32_t *idx, cudaStream_t st) {
+  int max_n = 0;
+  for (int b = 0; b < plan.nreq; ++b) max_n = max(max_n, plan.r[b].L - (plan.r[b].be - plan.r[b].bs));
+  const size_t smem = (size_t)max(max_n, 1) * sizeof(uint32_t);
+  cudaError_t e = cudaFuncSetAttribute(select_heads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  select_heads_kernel<<<plan.total_units, kSelThreads, smem, st>>>(plan, scores, idx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check_indices(const Plan &plan, const int32_t *idx, int32_t *violations,
+                                 cudaStream_t st) {
+  check_indices_kernel<<<plan.total_units, 256, 0, st>>>(plan, idx, violations);
+  return cudaGetLastError();
+}
+
+}  // namespace dllm

@@ -1,0 +1,244 @@
+"""Thin Python binding of libdllm's C-ABI (include/dllm.h).
+
+Argument marshalling only: every step of the path runs in libdllm's CUDA
+kernels.  Tensors are torch CUDA tensors (PyTorch supplies device memory and
+streams); host arrays are plain Python/numpy int sequences.  There is no CPU
+fallback: importing this module fails loudly if libdllm.so is missing, and a
+compute call on tensors that are not on a CUDA device raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdllm.so")
+
+DLLM_OK = 0
+DLLM_ERR_INVALID_ARG = -1
+DLLM_ERR_UNSUPPORTED = -2
+DLLM_ERR_SHAPE = -3
+DLLM_ERR_K_RANGE = -4
+DLLM_ERR_CUDA = -5
+
+EXPORTED = ("dllm_keep_count", "dllm_index_layout", "dllm_refresh_attn", "dllm_select_heads",
+            "dllm_reuse_sparse_attn", "dllm_check_indices", "dllm_status_string", "dllm_last_error",
+            "dllm_version")
+
+
+class DllmError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        super().__init__(f"{where}: {detail or ''} [{status_string(status)}]")
+        self.status = status
+
+
+class _Problem(ctypes.Structure):
+    _fields_ = [
+        ("num_requests", ctypes.c_int32),
+        ("num_heads", ctypes.c_int32),
+        ("num_kv_heads", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32),
+        ("seq_len", ctypes.POINTER(ctypes.c_int32)),
+        ("blk_start", ctypes.POINTER(ctypes.c_int32)),
+        ("blk_end", ctypes.POINTER(ctypes.c_int32)),
+        ("keep_ratio", ctypes.c_double),
+        ("pool_window", ctypes.c_int32),
+        ("softmax_scale", ctypes.c_float),
+        ("page_size", ctypes.c_int32),
+        ("pages_per_req", ctypes.c_int32),
+        ("block_table", ctypes.c_void_p),
+    ]
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libdllm.so not built ({LIB_PATH}); run `python -m paper_2512_17077_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER(_Problem)
+    vp = ctypes.c_void_p
+    lib.dllm_keep_count.argtypes = [ctypes.c_double, ctypes.c_int32]
+    lib.dllm_keep_count.restype = ctypes.c_int
+    lib.dllm_index_layout.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64),
+                                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+    lib.dllm_index_layout.restype = ctypes.c_int
+    lib.dllm_refresh_attn.argtypes = [P, vp, vp, vp, vp, vp, vp]
+    lib.dllm_refresh_attn.restype = ctypes.c_int
+    lib.dllm_select_heads.argtypes = [P, vp, vp, vp]
+    lib.dllm_select_heads.restype = ctypes.c_int
+    lib.dllm_reuse_sparse_attn.argtypes = [P, vp, vp, vp, vp, vp, vp]
+    lib.dllm_reuse_sparse_attn.restype = ctypes.c_int
+    lib.dllm_check_indices.argtypes = [P, vp, vp, vp]
+    lib.dllm_check_indices.restype = ctypes.c_int
+    lib.dllm_status_string.argtypes = [ctypes.c_int]
+    lib.dllm_status_string.restype = ctypes.c_char_p
+    lib.dllm_last_error.argtypes = []
+    lib.dllm_last_error.restype = ctypes.c_char_p
+    lib.dllm_version.argtypes = []
+    lib.dllm_version.restype = ctypes.c_char_p
+    return lib
+
+
+_lib = _load()
+
+
+def lib() -> ctypes.CDLL:
+    return _lib
+
+
+def status_string(status: int) -> str:
+    return _lib.dllm_status_string(status).decode()
+
+
+def last_error() -> str:
+    return _lib.dllm_last_error().decode()
+
+
+def version() -> str:
+    return _lib.dllm_version().decode()
+
+
+def _check(status: int, where: str) -> None:
+    if status != DLLM_OK:
+        raise DllmError(status, where, last_error())
+
+
+def keep_count(keep_ratio: float, n_ctx: int) -> int:
+    k = _lib.dllm_keep_count(float(keep_ratio), int(n_ctx))
+    _check(min(k, 0), "dllm_keep_count")
+    return k
+
+
+def _i32(xs) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(xs, dtype=np.int32))
+
+
+class Problem:
+    """Owns the host arrays and the device block table behind a dllm_problem."""
+
+    def __init__(self, seq_len: Sequence[int], blk_start: Sequence[int], blk_end: Sequence[int], *,
+                 num_heads: int, num_kv_heads: int, head_dim: int, keep_ratio: float, pool_window: int = 3,
+                 softmax_scale: float = 0.0, page_size: int = 64, block_table: Optional[torch.Tensor] = None,
+                 pages_per_req: Optional[int] = None):
+        self.seq_len, self.blk_start, self.blk_end = _i32(seq_len), _i32(blk_start), _i32(blk_end)
+        self.block_table = block_table
+        if pages_per_req is None:
+            pages_per_req = int(block_table.shape[1]) if block_table is not None and block_table.dim() == 2 else 0
+        self._s = _Problem()
+        s = self._s
+        s.num_requests = len(self.seq_len)
+        s.num_heads, s.num_kv_heads, s.head_dim = num_heads, num_kv_heads, head_dim
+        ptr = ctypes.POINTER(ctypes.c_int32)
+        s.seq_len = self.seq_len.ctypes.data_as(ptr)
+        s.blk_start = self.blk_start.ctypes.data_as(ptr)
+        s.blk_end = self.blk_end.ctypes.data_as(ptr)
+        s.keep_ratio = float(keep_ratio)
+        s.pool_window = int(pool_window)
+        s.softmax_scale = float(softmax_scale)
+        s.page_size = int(page_size)
+        s.pages_per_req = int(pages_per_req)
+        if block_table is not None:
+            assert block_table.dtype == torch.int32 and block_table.is_contiguous()
+            s.block_table = block_table.data_ptr()
+        else:
+            s.block_table = None
+
+    @property
+    def ref(self):
+        return ctypes.byref(self._s)
+
+    @property
+    def num_heads(self) -> int:
+        return self._s.num_heads
+
+    @property
+    def head_dim(self) -> int:
+        return self._s.head_dim
+
+    def layout(self):
+        """(k per request, total idx elements, total rows, total block rows)."""
+        B = self._s.num_requests
+        k = (ctypes.c_int32 * max(B, 1))()
+        ti, tr, tb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(_lib.dllm_index_layout(self.ref, k, ctypes.byref(ti), ctypes.byref(tr), ctypes.byref(tb)),
+               "dllm_index_layout")
+        return [k[i] for i in range(B)], ti.value, tr.value, tb.value
+
+
+def _dev(t: Optional[torch.Tensor], name: str, dtype=None) -> int:
+    if t is None:
+        return 0
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (libdllm has no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    return t.data_ptr()
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def refresh_attn(p: Problem, q, k_cache, v_cache, out, scores=None, stream=None) -> None:
+    """dllm_refresh_attn (Eq. 3 + Eq. 6 raw importance)."""
+    bf = torch.bfloat16
+    _check(_lib.dllm_refresh_attn(p.ref, _dev(q, "q", bf), _dev(k_cache, "k_cache", bf), _dev(v_cache, "v_cache", bf),
+                                  _dev(out, "out", bf), _dev(scores, "scores", torch.float32), _stream(stream)),
+           "dllm_refresh_attn")
+
+
+def select_heads(p: Problem, scores, idx, stream=None) -> None:
+    """dllm_select_heads (Eq. 6 pool + per-head TopK)."""
+    _check(_lib.dllm_select_heads(p.ref, _dev(scores, "scores", torch.float32), _dev(idx, "idx", torch.int32),
+                                  _stream(stream)), "dllm_select_heads")
+
+
+def reuse_sparse_attn(p: Problem, q_blk, k_cache, v_cache, idx, out_blk, stream=None) -> None:
+    """dllm_reuse_sparse_attn (Eq. 4 over per-head key subsets)."""
+    bf = torch.bfloat16
+    _check(_lib.dllm_reuse_sparse_attn(p.ref, _dev(q_blk, "q_blk", bf), _dev(k_cache, "k_cache", bf),
+                                       _dev(v_cache, "v_cache", bf), _dev(idx, "idx", torch.int32),
+                                       _dev(out_blk, "out_blk", bf), _stream(stream)), "dllm_reuse_sparse_attn")
+
+
+def check_indices(p: Problem, idx, violations, stream=None) -> None:
+    _check(_lib.dllm_check_indices(p.ref, _dev(idx, "idx", torch.int32), _dev(violations, "violations", torch.int32),
+                                   _stream(stream)), "dllm_check_indices")
+
+
+@dataclass
+class Buffers:
+    """Caller-owned outputs sized from dllm_index_layout."""
+    out: torch.Tensor
+    scores: torch.Tensor
+    idx: torch.Tensor
+    out_blk: torch.Tensor
+    k: list
+
+
+def alloc_buffers(p: Problem, device="cuda") -> Buffers:
+    k, total_idx, rows, blk_rows = p.layout()
+    H, D = p.num_heads, p.head_dim
+    return Buffers(
+        out=torch.empty((rows, H, D), dtype=torch.bfloat16, device=device),
+        scores=torch.empty((H * rows,), dtype=torch.float32, device=device),
+        idx=torch.empty((max(total_idx, 1),), dtype=torch.int32, device=device),
+        out_blk=torch.empty((blk_rows, H, D), dtype=torch.bfloat16, device=device),
+        k=k,
+    )
+
+
+def hot_path(p: Problem, q, q_blk, k_cache, v_cache, buf: Buffers, stream=None) -> None:
+    """One pass of the whole hot path: Refresh (+importance) -> select -> Reuse."""
+    refresh_attn(p, q, k_cache, v_cache, buf.out, buf.scores, stream)
+    select_heads(p, buf.scores, buf.idx, stream)
+    reuse_sparse_attn(p, q_blk, k_cache, v_cache, buf.idx, buf.out_blk, stream)

@@ -202,14 +202,17 @@ def _unpage(cache: torch.Tensor, row: torch.Tensor, L: int) -> torch.Tensor:
 
 
 def make_batch(wl: Workload, seed: Optional[int] = None, spare_pages: int = 3,
-               fill_nan: bool = True) -> Batch:
-    """All requests' tensors, packed (Q, Q_blk) and paged (K, V)."""
+               fill_nan: bool = True, page_seed: Optional[int] = None) -> Batch:
+    """All requests' tensors, packed (Q, Q_blk) and paged (K, V).
+
+    ``page_seed`` changes only the physical page permutation (same values)."""
     seed = base_seed() if seed is None else seed
+    page_seed = seed if page_seed is None else page_seed
     B, H, Hk, D, P = wl.num_requests, wl.num_heads, wl.num_kv_heads, wl.head_dim, wl.page_size
     npg = [(L + P - 1) // P for L in wl.seq_len]
     pages_per_req = max(npg)
     total_pages = sum(npg) + spare_pages
-    perm = torch.randperm(total_pages, generator=_gen(_subseed(seed, wl.name, "pages")))
+    perm = torch.randperm(total_pages, generator=_gen(_subseed(page_seed, wl.name, "pages")))
     fill = float("nan") if fill_nan else 0.0
     k_cache = torch.full((total_pages, Hk, P, D), fill, dtype=torch.bfloat16)
     v_cache = torch.full((total_pages, Hk, P, D), fill, dtype=torch.bfloat16)

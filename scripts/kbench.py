@@ -1,0 +1,83 @@
+"""Per-kernel timing on one config (dev tool; bench.py is the contract).
+
+    python scripts/kbench.py C1 [--iters 20] [--impl mma|tc]
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2512_17077_b200 import lib, synth  # noqa: E402
+
+
+def reuse_unique_bytes(wl, k, idx_flat):
+    g = wl.num_heads // wl.num_kv_heads
+    D = wl.head_dim
+    total, logical, off = 0, 0, 0
+    for b in range(wl.num_requests):
+        kb = k[b]
+        rows = idx_flat[off:off + wl.num_heads * kb].reshape(wl.num_heads, kb)
+        off += wl.num_heads * kb
+        blk = wl.blk_end[b] - wl.blk_start[b]
+        for kv in range(wl.num_kv_heads):
+            u = np.unique(rows[kv * g:(kv + 1) * g])
+            total += (len(u) + blk) * 2 * D * 2
+        logical += wl.num_heads * (kb + blk) * 2 * D * 2
+    extra = sum(wl.blk) * wl.num_heads * D * 2 * 2 + len(idx_flat) * 4
+    return total + extra, logical + extra
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("cfg", nargs="?", default="C1")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--r", type=float, default=None)
+    args = ap.parse_args()
+    wl = synth.config(args.cfg, keep_ratio=args.r)
+    batch = synth.make_batch(wl)
+    bt = batch.block_table.cuda()
+    p = lib.Problem(wl.seq_len, wl.blk_start, wl.blk_end, num_heads=wl.num_heads, num_kv_heads=wl.num_kv_heads,
+                    head_dim=wl.head_dim, keep_ratio=wl.keep_ratio, pool_window=wl.pool_window,
+                    page_size=wl.page_size, block_table=bt)
+    q, qb, kc, vc = batch.q.cuda(), batch.q_blk.cuda(), batch.k_cache.cuda(), batch.v_cache.cuda()
+    buf = lib.alloc_buffers(p)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    fns = {
+        "refresh": lambda: lib.refresh_attn(p, q, kc, vc, buf.out, buf.scores),
+        "select": lambda: lib.select_heads(p, buf.scores, buf.idx),
+        "reuse": lambda: lib.reuse_sparse_attn(p, qb, kc, vc, buf.idx, buf.out_blk),
+    }
+    for f in fns.values():
+        f()
+    torch.cuda.synchronize()
+    res = {}
+    for name, f in fns.items():
+        ts = []
+        for _ in range(args.iters):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            f()
+            e.record()
+            torch.cuda.synchronize()
+            ts.append(s.elapsed_time(e) * 1e-3)
+        res[name] = (np.median(ts), np.min(ts))
+    k, total_idx, rows, _ = p.layout()
+    flops = sum(4 * wl.num_heads * L * L * wl.head_dim for L in wl.seq_len)
+    ub, lb = reuse_unique_bytes(wl, k, buf.idx.cpu().numpy()[:total_idx])
+    sel_bytes = 4 * wl.num_heads * rows + 4 * total_idx
+    t = res["refresh"][0]
+    print(f"{args.cfg} refresh: {t*1e6:.1f} us  {flops/t/1e12:.1f} TFLOP/s (min {res['refresh'][1]*1e6:.1f})")
+    t = res["select"][0]
+    print(f"{args.cfg} select : {t*1e6:.1f} us  {sel_bytes/t/1e9:.1f} GB/s")
+    t = res["reuse"][0]
+    print(f"{args.cfg} reuse  : {t*1e6:.1f} us  {ub/t/1e9:.1f} GB/s unique ({lb/t/1e9:.1f} logical), "
+          f"unique {ub/1e6:.1f} MB")
+    print(lib.version())
+
+
+if __name__ == "__main__":
+    main()

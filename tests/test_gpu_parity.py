@@ -1,0 +1,323 @@
+"""GPU parity: the CUDA path through the C-ABI vs the fp64 oracle on the same
+seeded inputs (``-m gpu``).
+
+Contract (BASELINE.json north_star):
+  * selection indices bit-exact — (i) on generated fp32 score tensors fed to
+    both sides, (ii) end to end Refresh -> select on exact-integer Q/K,
+    (iii) on realistic inputs a valid top-k of the oracle's fp64 scores up to
+    the fp32 rounding bound;
+  * attention outputs within max-abs 1e-2 and mean-abs 1e-3 of the oracle.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2512_17077_b200 import synth
+from tests._util import (assert_close, f64, join_idx, join_scores, oracle_keep_counts, problem_of, split_idx,
+                         split_scores, to_dev)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def L():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from paper_2512_17077_b200 import lib
+    return lib
+
+
+def custom(name, L_, bs, be, H=4, Hk=2, D=128, r=0.25, w=3, P=64, kind="realistic"):
+    return synth.Workload(name, H, Hk, D, list(L_), list(bs), list(be), r, w, P, kind)
+
+
+EDGE = {
+    "single_token": custom("e_single", [1], [0], [1], H=2, Hk=2, D=64),
+    "block_whole_seq": custom("e_whole", [40], [0], [40], H=2, Hk=1, D=64),
+    "block_first": custom("e_first", [64], [0], [8], H=2, Hk=2, D=16, P=16),
+    "block_last": custom("e_last", [64], [56], [64], H=2, Hk=2, D=16, P=16),
+    "ragged_straddle": custom("e_strad", [100, 77], [60, 10], [70, 42], H=4, Hk=4, D=128),
+    "blk128_straddle": custom("e_b128", [300], [100], [228], H=2, Hk=1, D=128),
+    "blk1_mid": custom("e_blk1", [513], [200], [201], H=4, Hk=2, D=64, P=256),
+    "gqa_d32_p16": custom("e_gqa", [130, 257, 64], [64, 225, 0], [96, 257, 32], H=8, Hk=2, D=32, P=16),
+    "r1_dense": custom("e_r1", [192], [96], [128], H=2, Hk=2, D=128, r=1.0),
+    "tiny_r_w5": custom("e_tiny", [333], [300], [332], H=3, Hk=1, D=64, r=0.001, w=5),
+    "w1": custom("e_w1", [129], [64], [96], H=2, Hk=2, D=128, w=1),
+}
+
+
+def _run_refresh(L, batch, with_scores=True):
+    p = problem_of(batch)
+    q, q_blk, kc, vc = to_dev(batch)
+    k, total_idx, rows, blk_rows = p.layout()
+    wl = batch.wl
+    out = torch.full((rows, wl.num_heads, wl.head_dim), float("nan"), dtype=torch.bfloat16, device="cuda")
+    sc = torch.full((wl.num_heads * rows,), float("nan"), dtype=torch.float32, device="cuda") if with_scores else None
+    L.refresh_attn(p, q, kc, vc, out, sc)
+    torch.cuda.synchronize()
+    return p, out.float().cpu().numpy(), (sc.cpu().numpy() if with_scores else None)
+
+
+def _run_select(L, p, scores_flat):
+    k, total_idx, rows, blk_rows = p.layout()
+    idx = torch.full((max(total_idx, 1),), -7, dtype=torch.int32, device="cuda")
+    L.select_heads(p, torch.from_numpy(np.ascontiguousarray(scores_flat, dtype=np.float32)).cuda(), idx)
+    torch.cuda.synchronize()
+    return k, idx.cpu().numpy()[:total_idx]
+
+
+def _run_reuse(L, batch, p, idx_flat):
+    q, q_blk, kc, vc = to_dev(batch)
+    k, total_idx, rows, blk_rows = p.layout()
+    wl = batch.wl
+    out = torch.full((blk_rows, wl.num_heads, wl.head_dim), float("nan"), dtype=torch.bfloat16, device="cuda")
+    idx = torch.from_numpy(np.ascontiguousarray(idx_flat, dtype=np.int32)).cuda() if len(idx_flat) else \
+        torch.zeros(1, dtype=torch.int32, device="cuda")
+    L.reuse_sparse_attn(p, q_blk, kc, vc, idx, out)
+    torch.cuda.synchronize()
+    return out.float().cpu().numpy()
+
+
+def _oracle_refresh(batch, b):
+    wl = batch.wl
+    q, K, V = f64(batch.q_req(b)), f64(batch.k_logical(b)), f64(batch.v_logical(b))
+    return O.attention_dense(q, K, V), O.raw_scores(q[wl.blk_start[b]:wl.blk_end[b]], K)
+
+
+def _check_refresh(batch, out, scores, requests=None):
+    wl = batch.wl
+    sc = split_scores(scores, wl) if scores is not None else None
+    for b in (range(wl.num_requests) if requests is None else requests):
+        o_ref, raw_ref = _oracle_refresh(batch, b)
+        c0, c1 = batch.cu_seqlens[b], batch.cu_seqlens[b + 1]
+        assert_close(out[c0:c1], o_ref, f"{wl.name} refresh out req {b}")
+        if sc is not None:
+            # fp32 tensor-core accumulation vs fp64: |err| <= D * 2^-22 * sum|q k|
+            q, K = f64(batch.q_req(b)), f64(batch.k_logical(b))
+            qb = np.abs(q[wl.blk_start[b]:wl.blk_end[b]])
+            bound = wl.head_dim * 2.0 ** -22 * np.stack(
+                [(qb[:, h] @ np.abs(K[:, h // (wl.num_heads // wl.num_kv_heads)]).T).max(axis=0)
+                 for h in range(wl.num_heads)]) + 1e-6
+            err = np.abs(sc[b] - raw_ref)
+            assert (err <= bound).all(), f"{wl.name} scores req {b}: max err {err.max():.3e}"
+
+
+# ------------------------------------------------------------------ select (i)
+SELECT_CASES = [("C0", None, None), ("C1", None, None), ("C2", None, None), ("C3", None, 24),
+                ("C4", 0.05, 3), ("C4", 0.5, 3), ("C4", 1.0, 2)]
+
+
+@pytest.mark.parametrize("mode", ["ties", "normal", "wide"])
+@pytest.mark.parametrize("cfg,r,n", SELECT_CASES)
+def test_select_bitexact_on_generated_scores(L, cfg, r, n, mode):
+    wl = synth.config(cfg, keep_ratio=r, num_requests=n)
+    batch_bt = torch.zeros((wl.num_requests, 1), dtype=torch.int32)
+    p = L.Problem(wl.seq_len, wl.blk_start, wl.blk_end, num_heads=wl.num_heads, num_kv_heads=wl.num_kv_heads,
+                  head_dim=wl.head_dim, keep_ratio=wl.keep_ratio, pool_window=wl.pool_window,
+                  page_size=1024, block_table=batch_bt.cuda(), pages_per_req=8)
+    sc = synth.scores(wl, mode=mode)
+    k, got = _run_select(L, p, join_scores(sc))
+    assert k == oracle_keep_counts(wl)
+    ref = O.select_batch([s.astype(np.float64) for s in sc], wl.seq_len, wl.blk_start, wl.blk_end,
+                         wl.keep_ratio, wl.pool_window)
+    assert np.array_equal(got, join_idx(ref)), f"{cfg}/{mode}: selection differs"
+
+
+@pytest.mark.parametrize("w", [1, 5, 7])
+def test_select_windows(L, w):
+    wl = synth.config("C1", num_requests=4)
+    wl.pool_window = w
+    p = L.Problem(wl.seq_len, wl.blk_start, wl.blk_end, num_heads=32, num_kv_heads=32, head_dim=128,
+                  keep_ratio=0.25, pool_window=w, page_size=64,
+                  block_table=torch.zeros((4, 16), dtype=torch.int32).cuda())
+    sc = synth.scores(wl, mode="ties")
+    k, got = _run_select(L, p, join_scores(sc))
+    ref = O.select_batch([s.astype(np.float64) for s in sc], wl.seq_len, wl.blk_start, wl.blk_end, 0.25, w)
+    assert np.array_equal(got, join_idx(ref))
+
+
+# ------------------------------------------------------------------ refresh
+@pytest.mark.parametrize("cfg,n", [("C0", None), ("C1", 2), ("C2", 2)])
+def test_refresh_parity_configs(L, cfg, n):
+    batch = synth.make_batch(synth.config(cfg, num_requests=n))
+    p, out, scores = _run_refresh(L, batch)
+    _check_refresh(batch, out, scores)
+
+
+@pytest.mark.parametrize("name", sorted(EDGE))
+def test_refresh_parity_edges(L, name):
+    batch = synth.make_batch(EDGE[name])
+    p, out, scores = _run_refresh(L, batch)
+    _check_refresh(batch, out, scores)
+    # without scores the outputs are identical
+    p2, out2, _ = _run_refresh(L, batch, with_scores=False)
+    assert np.array_equal(out, out2)
+
+
+# ------------------------------------------------------------------ selection (ii): exact end to end
+def _exact(wl):
+    wl = synth.Workload(**{**wl.__dict__, "kind": "exact"})
+    return wl
+
+
+@pytest.mark.parametrize("cfg,n", [("C0", None), ("C1", 2), ("C2", 2), ("C3", 3)])
+def test_selection_end_to_end_exact(L, cfg, n):
+    batch = synth.make_batch(synth.config(cfg, num_requests=n, kind="exact"))
+    p, out, scores = _run_refresh(L, batch)
+    k, got = _run_select(L, p, scores)
+    wl = batch.wl
+    ref = [O.select_heads(f64(batch.q_req(b))[wl.blk_start[b]:wl.blk_end[b]], f64(batch.k_logical(b)),
+                          wl.seq_len[b], wl.blk_start[b], wl.blk_end[b], wl.keep_ratio, wl.pool_window)
+           for b in range(wl.num_requests)]
+    assert np.array_equal(got, join_idx(ref))
+
+
+@pytest.mark.parametrize("name", sorted(EDGE))
+def test_selection_end_to_end_exact_edges(L, name):
+    batch = synth.make_batch(_exact(EDGE[name]))
+    p, out, scores = _run_refresh(L, batch)
+    k, got = _run_select(L, p, scores)
+    wl = batch.wl
+    assert k == oracle_keep_counts(wl)
+    ref = [O.select_heads(f64(batch.q_req(b))[wl.blk_start[b]:wl.blk_end[b]], f64(batch.k_logical(b)),
+                          wl.seq_len[b], wl.blk_start[b], wl.blk_end[b], wl.keep_ratio, wl.pool_window)
+           for b in range(wl.num_requests)]
+    assert np.array_equal(got, join_idx(ref))
+
+
+# ------------------------------------------------------------------ reuse
+def _check_reuse(batch, got, idx_list, requests=None):
+    wl = batch.wl
+    for b in (range(wl.num_requests) if requests is None else requests):
+        ref = O.attention_with_cache(f64(batch.q_blk_req(b)), f64(batch.k_logical(b)), f64(batch.v_logical(b)),
+                                     wl.blk_start[b], wl.blk_end[b], idx_list[b])
+        c0, c1 = batch.cu_blk[b], batch.cu_blk[b + 1]
+        assert_close(got[c0:c1], ref, f"{wl.name} reuse req {b}")
+
+
+@pytest.mark.parametrize("mode", ["random", "shared"])
+@pytest.mark.parametrize("cfg,n", [("C0", None), ("C1", 4), ("C2", 4), ("C3", 6)])
+def test_reuse_parity_generated_indices(L, cfg, n, mode):
+    batch = synth.make_batch(synth.config(cfg, num_requests=n))
+    p = problem_of(batch)
+    k = oracle_keep_counts(batch.wl)
+    assert k == p.layout()[0]
+    idx = synth.indices(batch.wl, k, mode=mode)
+    got = _run_reuse(L, batch, p, join_idx(idx))
+    _check_reuse(batch, got, idx)
+
+
+@pytest.mark.parametrize("name", sorted(EDGE))
+def test_reuse_parity_edges(L, name):
+    batch = synth.make_batch(EDGE[name])
+    p = problem_of(batch)
+    k = oracle_keep_counts(batch.wl)
+    idx = synth.indices(batch.wl, k)
+    got = _run_reuse(L, batch, p, join_idx(idx))
+    _check_reuse(batch, got, idx)
+
+
+def test_reuse_r1_equals_refresh_rows(L):
+    """keep ratio 1 + Q_blk = Q[bs:be]: Reuse rows == Refresh rows."""
+    wl = custom("e_r1eq", [320, 200], [128, 40], [160, 72], H=4, Hk=2, D=128, r=1.0)
+    batch = synth.make_batch(wl)
+    batch.q_blk = torch.cat([batch.q_req(b)[wl.blk_start[b]:wl.blk_end[b]] for b in range(2)])
+    p, out, scores = _run_refresh(L, batch)
+    k, idx = _run_select(L, p, scores)
+    got = _run_reuse(L, batch, p, idx)
+    for b in range(2):
+        ref = out[batch.cu_seqlens[b] + wl.blk_start[b]: batch.cu_seqlens[b] + wl.blk_end[b]]
+        d = np.abs(got[batch.cu_blk[b]:batch.cu_blk[b + 1]] - ref)
+        assert d.max() <= 1.6e-2 and d.mean() <= 1e-3
+
+
+# ------------------------------------------------------------------ end to end (iii), determinism
+def test_end_to_end_realistic_selection_valid(L):
+    batch = synth.make_batch(synth.config("C1", num_requests=2))
+    wl = batch.wl
+    p, out, scores = _run_refresh(L, batch)
+    k, got = _run_select(L, p, scores)
+    got_l = split_idx(got, wl, k)
+    mism = 0
+    for b in range(wl.num_requests):
+        q, K = f64(batch.q_req(b)), f64(batch.k_logical(b))
+        bs, be, Lb = wl.blk_start[b], wl.blk_end[b], wl.seq_len[b]
+        C = O.candidates(Lb, bs, be)
+        S = O.pool_scores(O.raw_scores(q[bs:be], K[C]), wl.pool_window)
+        ref = O.select_heads(q[bs:be], K, Lb, bs, be, wl.keep_ratio, wl.pool_window)
+        pos2c = {int(c): i for i, c in enumerate(C)}
+        for h in range(wl.num_heads):
+            eps = wl.head_dim * 2.0 ** -22 * np.abs(q[bs:be, h]).max() * np.abs(K[C, h]).sum(axis=1).max() + 1e-6
+            gs, rs = set(got_l[b][h].tolist()), set(ref[h].tolist())
+            for a, c in zip(sorted(gs - rs), sorted(rs - gs)):
+                assert abs(S[h, pos2c[a]] - S[h, pos2c[c]]) <= 2 * eps
+                mism += 1
+    assert mism <= 4, f"{mism} rounding-level selection flips"
+    # Reuse with the selected lists (only compared where the selection is exact)
+    gotr = _run_reuse(L, batch, p, got)
+    _check_reuse(batch, gotr, got_l)
+
+
+def test_determinism_and_page_permutation_invariance(L):
+    wl = synth.config("C2", num_requests=2)
+    b1 = synth.make_batch(wl)
+    b2 = synth.make_batch(wl, page_seed=12345)
+    assert not torch.equal(b1.block_table, b2.block_table)
+    res = []
+    for bb in (b1, b1, b2):
+        p, out, scores = _run_refresh(L, bb)
+        k, idx = _run_select(L, p, scores)
+        ob = _run_reuse(L, bb, p, idx)
+        res.append((out, scores, idx, ob))
+    for other in res[1:]:
+        for a, b in zip(res[0], other):
+            assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+def test_check_indices(L):
+    batch = synth.make_batch(synth.config("C1", num_requests=3))
+    p = problem_of(batch)
+    k = p.layout()[0]
+    idx = join_idx(synth.indices(batch.wl, k))
+    viol = torch.zeros(1, dtype=torch.int32, device="cuda")
+    L.check_indices(p, torch.from_numpy(idx).cuda(), viol)
+    torch.cuda.synchronize()
+    assert int(viol.item()) == 0
+    bad = idx.copy()
+    bad[5] = batch.wl.blk_start[0]          # inside the block
+    bad[k[0] * 3 + 7] = 10 ** 6             # out of range (and breaks ascending order)
+    L.check_indices(p, torch.from_numpy(bad).cuda(), viol)
+    torch.cuda.synchronize()
+    assert int(viol.item()) >= 2
+
+
+# ------------------------------------------------------------------ full-size configs, sampled outputs
+@pytest.mark.parametrize("cfg,sample", [("C1", [0, 9, 15]), ("C2", [0, 31])])
+def test_full_config_hot_path_sampled(L, cfg, sample):
+    """BASELINE sizes, the launch configuration bench.py times: whole batch on the
+    GPU, oracle on sampled requests (exact-integer Q/K so the selection is bit-exact)."""
+    wl = synth.config(cfg, kind="exact")
+    batch = synth.make_batch(wl)
+    p = problem_of(batch)
+    q, q_blk, kc, vc = to_dev(batch)
+    buf = L.alloc_buffers(p)
+    L.hot_path(p, q, q_blk, kc, vc, buf)
+    torch.cuda.synchronize()
+    out = buf.out.float().cpu().numpy()
+    k, total_idx, rows, blk_rows = p.layout()
+    idx = split_idx(buf.idx.cpu().numpy()[:total_idx], wl, k)
+    ob = buf.out_blk.float().cpu().numpy()
+    for b in sample:
+        qb, K, V = f64(batch.q_req(b)), f64(batch.k_logical(b)), f64(batch.v_logical(b))
+        bs, be = wl.blk_start[b], wl.blk_end[b]
+        c0, c1 = batch.cu_seqlens[b], batch.cu_seqlens[b + 1]
+        # exact-integer logits are large; compare Refresh on a row sample with the stated tolerance
+        rows_s = np.r_[0:4, bs:be, wl.seq_len[b] - 4:wl.seq_len[b]]
+        ref = O.attention_dense(qb[rows_s], K, V)
+        assert_close(out[c0:c1][rows_s], ref, f"{cfg} refresh req {b}")
+        sel = O.select_heads(qb[bs:be], K, wl.seq_len[b], bs, be, wl.keep_ratio, wl.pool_window)
+        assert np.array_equal(idx[b], sel), f"{cfg} selection req {b}"
+        ref_u = O.attention_with_cache(f64(batch.q_blk_req(b)), K, V, bs, be, sel)
+        assert_close(ob[batch.cu_blk[b]:batch.cu_blk[b + 1]], ref_u, f"{cfg} reuse req {b}")
