@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark of the Head-Centric Sparse Attention hot path (one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (one process per GPU, NCCL)
+
+A step = one pass of the whole hot path over one batch:
+dllm_refresh_attn (Eq. 3 + importance) -> dllm_select_heads (Eq. 6 + TopK) ->
+dllm_reuse_sparse_attn (Eq. 4), through the C-ABI.  At N=1 the batch is
+BASELINE.json configs[1] (C1, LLaDA-8B layer shape: 16 requests, 32 heads,
+D=128, L=1024, block 32, keep 0.25).  At N>1 every rank runs its LPT shard of
+an N-times-replicated batch (weak scaling: 16 requests per GPU); there is no
+collective on the data path (requests are independent).  The NCCL all-gather
+of the per-request outputs is timed separately (`allgather_ms`).
+
+value  = requests/s over all ranks = (requests per step * K) / max-over-ranks
+         device time of the K steps (CUDA events on the launch stream; L2
+         flushed before every step by a 512 MiB write outside the events).
+e2e    = the same metric through the public API with HOST buffers: every step
+         copies its inputs from pinned host memory to the device, runs the
+         three calls and copies the results back (all inside the events).
+roofline = the dominant kernel (Refresh, tensor-bound) against the measured
+         bf16 peak in MEASURED_PEAKS.json; Reuse / select are reported in
+         `kernels` against the measured HBM copy bandwidth.
+cpu_baseline = the fp64 oracle (oracle/) timed on this host's cores on a
+         bounded sample of the same workload (rank 0, N=1 only).
+--impl reference runs that oracle as the reference arm (BASELINE has no
+         runnable reference implementation: the paper ships no code).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Reuse sparse-attn HBM GB/s and Refresh TFLOPS vs peak; requests/s at 1/2/4/8 B200"
+UNIT = "requests/s"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk["bf16_tflops"], pk.get("bf16_tflops_sustained"), pk["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def workload_desc(wl, n):
+    return (f"{wl.name}: {wl.num_requests} requests/GPU x {n} GPU, H={wl.num_heads}, H_kv={wl.num_kv_heads}, "
+            f"D={wl.head_dim}, L={min(wl.seq_len)}..{max(wl.seq_len)}, blk={wl.blk[0]}, r={wl.keep_ratio}, "
+            f"w={wl.pool_window}, page={wl.page_size}")
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.samples, self._stop = index, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
+                          and not s[2 + i].startswith("Not")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) timing
+def cpu_oracle_rate(wl, budget_s: float = 12.0, max_requests: int | None = None):
+    """The fp64 oracle as it stands, on a bounded sample of the workload's
+    requests (whole requests: Refresh + importance + select + Reuse, all heads).
+    Returns (requests/s, requests timed, seconds, threads)."""
+    import torch
+
+    import oracle as O
+    from paper_2512_17077_b200 import synth
+    cores = len(os.sched_getaffinity(0))
+    torch.set_num_threads(cores)
+    done, t_total = 0, 0.0
+    b = 0
+    while b < wl.num_requests and (max_requests is None or done < max_requests):
+        q, K, V, qb = (t.double().numpy() for t in synth.request_tensors(wl, b))
+        bs, be, L = wl.blk_start[b], wl.blk_end[b], wl.seq_len[b]
+        t0 = time.perf_counter()
+        O.attention_dense(q, K, V)
+        raw = O.raw_scores(q[bs:be], K)
+        sel = O.select_batch([raw], [L], [bs], [be], wl.keep_ratio, wl.pool_window)[0]
+        O.attention_with_cache(qb, K, V, bs, be, sel)
+        t_total += time.perf_counter() - t0
+        done += 1
+        b += 1
+        if t_total >= budget_s:
+            break
+    return done / t_total, done, t_total, cores
+
+
+# ----------------------------------------------------------------------------- ncu traffic
+def ncu_traffic(kernel: str, cfg: str):
+    """dram read+write bytes per launch from the committed `ncu --set full`
+    summary (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        e = d.get(cfg, {}).get(kernel)
+        return None if e is None else e.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2512_17077_b200 import synth
+    wl = synth.config(args.config)
+    rates = []
+    for _ in range(args.warmup):
+        cpu_oracle_rate(wl, budget_s=0.0, max_requests=1)
+    t0 = time.perf_counter()
+    n_req = 0
+    for _ in range(args.steps):
+        r, n, t, cores = cpu_oracle_rate(wl, budget_s=0.0, max_requests=1)
+        rates.append(r)
+        n_req += n
+    wall = time.perf_counter() - t0
+    value = n_req / wall
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(wl, 1), "sample": "1 request (all heads) per step"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+                             "sample": f"{args.steps} steps x 1 request of {wl.name} (Refresh+select+Reuse, all heads)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C1")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_17077_b200 import lib, shard, synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    tf_peak, tf_sust, hbm_peak, peak_src = load_peaks()
+
+    base = synth.config(args.config)
+    glob = synth.replicate(base, world)
+    k_glob = [lib.keep_count(glob.keep_ratio, L - (e - s)) for L, s, e in zip(glob.seq_len, glob.blk_start, glob.blk_end)]
+    costs = [shard.request_cost(L, e - s, glob.num_heads, glob.num_kv_heads, glob.head_dim, k)
+             for L, s, e, k in zip(glob.seq_len, glob.blk_start, glob.blk_end, k_glob)]
+    parts = shard.lpt_partition(costs, world)
+    wl = synth.subset(glob, parts[rank])
+    batch = synth.make_batch(wl)
+
+    p = lib.Problem(wl.seq_len, wl.blk_start, wl.blk_end, num_heads=wl.num_heads, num_kv_heads=wl.num_kv_heads,
+                    head_dim=wl.head_dim, keep_ratio=wl.keep_ratio, pool_window=wl.pool_window,
+                    page_size=wl.page_size, block_table=batch.block_table.to(dev))
+    q, qb, kc, vc = (t.to(dev) for t in (batch.q, batch.q_blk, batch.k_cache, batch.v_cache))
+    buf = lib.alloc_buffers(p, device=dev)
+    k, total_idx, rows, blk_rows = p.layout()
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    n_launch_per_call = (wl.num_requests + 255) // 256
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        lib.refresh_attn(p, q, kc, vc, buf.out, buf.scores, stream)
+        if ev is not None:
+            ev[1].record(stream)
+        lib.select_heads(p, buf.scores, buf.idx, stream)
+        if ev is not None:
+            ev[2].record(stream)
+        lib.reuse_sparse_attn(p, qb, kc, vc, buf.idx, buf.out_blk, stream)
+        if ev is not None:
+            ev[3].record(stream)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize(dev)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local_rank) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            step(evs[i])
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    t_ref = [evs[i][0].elapsed_time(evs[i][1]) * 1e-3 for i in range(args.steps)]
+    t_sel = [evs[i][1].elapsed_time(evs[i][2]) * 1e-3 for i in range(args.steps)]
+    t_reu = [evs[i][2].elapsed_time(evs[i][3]) * 1e-3 for i in range(args.steps)]
+    t_step = [evs[i][0].elapsed_time(evs[i][3]) * 1e-3 for i in range(args.steps)]
+    total = sum(t_step)
+    tt = torch.tensor([total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    total_max = float(tt.item())
+    reqs_per_step = glob.num_requests
+    value = reqs_per_step * args.steps / total_max
+
+    # ---- algorithmic work per launch
+    H, Hk, D = wl.num_heads, wl.num_kv_heads, wl.head_dim
+    flops_refresh = sum(4.0 * H * L * L * D for L in wl.seq_len)
+    idx_host = buf.idx[:total_idx].cpu().numpy()
+    g = H // Hk
+    uniq_rows, off = 0, 0
+    for b in range(wl.num_requests):
+        rows_b = idx_host[off:off + H * k[b]].reshape(H, k[b])
+        off += H * k[b]
+        for kv in range(Hk):
+            uniq_rows += len(np.unique(rows_b[kv * g:(kv + 1) * g])) + wl.blk[b]
+    reuse_bytes = uniq_rows * 2 * D * 2 + 2 * blk_rows * H * D * 2 + 4 * total_idx
+    reuse_logical = sum(H * (wl.blk[b] + k[b]) for b in range(wl.num_requests)) * 2 * D * 2 + \
+        2 * blk_rows * H * D * 2 + 4 * total_idx
+    select_bytes = 4 * H * rows + 4 * total_idx
+    a_ref = flops_refresh / statistics.mean(t_ref) / 1e12
+    a_reu = reuse_bytes / statistics.mean(t_reu) / 1e9
+    a_sel = select_bytes / statistics.mean(t_sel) / 1e9
+
+    # ---- all-gather of per-request outputs (NCCL), timed separately
+    allgather_ms = None
+    if world > 1:
+        counts_rows = [sum(glob.seq_len[i] for i in parts[r]) for r in range(world)]
+        counts_blk = [sum(glob.blk[i] for i in parts[r]) for r in range(world)]
+        for _ in range(2):
+            shard.allgather_outputs(buf.out, counts_rows)
+            shard.allgather_outputs(buf.out_blk, counts_blk)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        shard.allgather_outputs(buf.out, counts_rows)
+        shard.allgather_outputs(buf.out_blk, counts_blk)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ag = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(ag, op=dist.ReduceOp.MAX)
+        allgather_ms = float(ag.item())
+
+    # ---- end to end through the public API with host buffers
+    pin = lambda t: t.pin_memory()  # noqa: E731
+    h_in = [pin(batch.q), pin(batch.q_blk), pin(batch.k_cache), pin(batch.v_cache)]
+    h_out = [torch.empty(buf.out.shape, dtype=buf.out.dtype).pin_memory(),
+             torch.empty(buf.out_blk.shape, dtype=buf.out_blk.dtype).pin_memory(),
+             torch.empty((max(total_idx, 1),), dtype=torch.int32).pin_memory()]
+    d_in = [q, qb, kc, vc]
+    h2d = sum(t.numel() * t.element_size() for t in h_in)
+    d2h = sum(t.numel() * t.element_size() for t in h_out)
+
+    def e2e_step():
+        for d, h in zip(d_in, h_in):
+            d.copy_(h, non_blocking=True)
+        step()
+        h_out[0].copy_(buf.out, non_blocking=True)
+        h_out[1].copy_(buf.out_blk, non_blocking=True)
+        h_out[2].copy_(buf.idx[:max(total_idx, 1)], non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    te = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = reqs_per_step * args.e2e_steps / float(te.item())
+
+    # ---- CPU oracle baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r, n, t, cores = cpu_oracle_rate(base, budget_s=12.0)
+        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{n} of {base.num_requests} {base.name} requests (Refresh+importance+select+Reuse, "
+                         f"all heads, fp64 numpy), {t:.1f} s"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        traffic = ncu_traffic("refresh", args.config)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": workload_desc(base, world), "global_requests": reqs_per_step,
+                       "parallelism": f"request-sharded dp{world} (LPT), no data-path collective",
+                       "l2": "flushed before every step (512 MiB write, outside the step events)",
+                       "seed": synth.base_seed()},
+            "roofline": {"bound": "tensor", "kernel": "dllm_refresh_attn (tcgen05)", "achieved": a_ref,
+                         "peak": tf_peak, "unit": "TFLOP/s", "frac": a_ref / tf_peak, "traffic": traffic,
+                         "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
+                         "frac_of_sustained": (a_ref / tf_sust) if tf_sust else None},
+            "kernels": {
+                "refresh": {"us": 1e6 * statistics.mean(t_ref), "TFLOP/s": a_ref, "frac": a_ref / tf_peak,
+                            "flop_per_launch": flops_refresh},
+                "select": {"us": 1e6 * statistics.mean(t_sel), "GB/s": a_sel, "frac": a_sel / hbm_peak,
+                           "bytes_per_launch": select_bytes},
+                "reuse": {"us": 1e6 * statistics.mean(t_reu), "GB/s": a_reu, "frac": a_reu / hbm_peak,
+                          "bytes_per_launch_unique": reuse_bytes, "bytes_per_launch_logical": reuse_logical,
+                          "GB/s_logical": reuse_logical / statistics.mean(t_reu) / 1e9, "bound": "hbm",
+                          "peak": hbm_peak},
+                "block_cycle_us": 1e6 * (statistics.mean(t_ref) + statistics.mean(t_sel) + 31 * statistics.mean(t_reu)),
+            },
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": 3 * n_launch_per_call * args.steps,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+            "allgather_ms": allgather_ms,
+            "lib": lib.version(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

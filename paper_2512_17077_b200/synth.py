@@ -34,7 +34,7 @@ import numpy as np
 import torch
 
 __all__ = ["Workload", "config", "CONFIG_NAMES", "request_tensors", "Batch", "make_batch",
-           "indices", "scores"]
+           "indices", "scores", "replicate", "subset"]
 
 
 def _subseed(*parts) -> int:
@@ -62,6 +62,8 @@ class Workload:
     kind: str = "realistic"       # or "exact"
     # for mixed batches (C3): which requests run Refresh (+select); the rest Reuse only
     refresh_mask: Optional[List[bool]] = None
+    # global request ids (seeding) when this workload is a shard / replica of another
+    req_ids: Optional[List[int]] = None
 
     @property
     def num_requests(self) -> int:
@@ -134,6 +136,25 @@ def config(name: str, seed: Optional[int] = None, keep_ratio: Optional[float] = 
     return wl
 
 
+def replicate(wl: Workload, n: int) -> Workload:
+    """n copies of a batch (weak scaling): replica 0 is bit-identical to ``wl``,
+    replica r draws its own values (request ids offset by r * B)."""
+    B = wl.num_requests
+    ids = [r * B + b for r in range(n) for b in range(B)]
+    mask = None if wl.refresh_mask is None else wl.refresh_mask * n
+    return Workload(wl.name, wl.num_heads, wl.num_kv_heads, wl.head_dim, wl.seq_len * n, wl.blk_start * n,
+                    wl.blk_end * n, wl.keep_ratio, wl.pool_window, wl.page_size, wl.kind, mask, ids)
+
+
+def subset(wl: Workload, reqs: Sequence[int]) -> Workload:
+    """The requests ``reqs`` of ``wl`` (a rank's shard); values are unchanged."""
+    rid = wl.req_ids if wl.req_ids is not None else list(range(wl.num_requests))
+    pick = lambda xs: [xs[i] for i in reqs]  # noqa: E731
+    return Workload(wl.name, wl.num_heads, wl.num_kv_heads, wl.head_dim, pick(wl.seq_len), pick(wl.blk_start),
+                    pick(wl.blk_end), wl.keep_ratio, wl.pool_window, wl.page_size, wl.kind,
+                    None if wl.refresh_mask is None else pick(wl.refresh_mask), pick(rid))
+
+
 def _bf16(x: torch.Tensor) -> torch.Tensor:
     return x.to(torch.bfloat16)
 
@@ -153,7 +174,8 @@ def request_tensors(wl: Workload, b: int, seed: Optional[int] = None):
     seed = base_seed() if seed is None else seed
     L, H, Hk, D = wl.seq_len[b], wl.num_heads, wl.num_kv_heads, wl.head_dim
     blk = wl.blk_end[b] - wl.blk_start[b]
-    tag = (seed, wl.name, wl.kind, b, L, H, Hk, D)
+    rid = wl.req_ids[b] if wl.req_ids is not None else b
+    tag = (seed, wl.name, wl.kind, rid, L, H, Hk, D)
 
     def qk(shape, t):
         g = _gen(_subseed(*tag, t))
