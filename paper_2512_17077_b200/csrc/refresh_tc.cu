@@ -145,9 +145,12 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t *>(gb + C::kOffBar + 8 * B_TMEMSLOT);
+  // register rebalancing (per role branch): the producer / MMA warpgroup needs
+  // few registers, the softmax warpgroups hold a full 128-column S row per thread
 
   if (warp == 0) {
     // ============================ TMA producer ============================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;\n" ::: "memory");
     int it = 0, ucnt = 0;
     const int boxrows = plan.page_size < TBN ? plan.page_size : TBN;
     const int nsub = TBN / boxrows;
@@ -215,6 +218,7 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
     }
   } else if (warp == 1) {
     // ============================ MMA issuer ============================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;\n" ::: "memory");
     if (lane == 0) {
       constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(TBM, TBN, false, false);
       constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(TBM, D, false, true);
@@ -295,8 +299,11 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
       }
     }
     __syncwarp();
-  } else if (warp >= 4) {
+  } else if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;\n" ::: "memory");
+  } else {
     // ============================ softmax warpgroups ============================
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 192;\n" ::: "memory");
     const int wg = (warp - 4) >> 2;
     const int wq = warp & 3;                       // TMEM lane quarter
     const int row = wq * 32 + lane;                // row of the Q tile == TMEM lane
@@ -366,9 +373,20 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
               if (c >= key_end) s[c] = -INFINITY;
           }
         }
-        float mx = s[0];
+        // row max: 8 independent 3-input max chains, then a tree
+        float mx;
+        {
+          float t[8];
 #pragma unroll
-        for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
+          for (int i = 0; i < 8; ++i) t[i] = fmax3(s[i], s[8 + i], s[16 + i]);
+#pragma unroll
+          for (int c = 24; c < 120; c += 16)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) t[i] = fmax3(t[i], s[c + i], s[c + 8 + i]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) t[i] = fmaxf(t[i], s[120 + i]);
+          mx = fmax3(fmax3(t[0], t[1], t[2]), fmax3(t[3], t[4], t[5]), fmaxf(t[6], t[7]));
+        }
         mx *= sl2;
         // lazy rescale; tcgen05.ld/st are warp-collective, so the decision is warp-uniform
         const bool need = j > 0 && mx > m_used + kRescaleLog2;
@@ -389,16 +407,32 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
             DLLM_TMEM_ST32(tO + c, o);
           }
         }
-        uint32_t pk[64];
+        // P = exp2(s * tau*log2e - m) in packed fp32x2 FMA + MUFU, bf16 pairs to TMEM
+        {
+          const uint64_t sl2x2 = pack_f32x2(sl2, sl2);
+          const uint64_t negm = pack_f32x2(-m_used, -m_used);
+          uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const float p0 = fast_exp2(fmaf(s[2 * c], sl2, -m_used));
-          const float p1 = fast_exp2(fmaf(s[2 * c + 1], sl2, -m_used));
-          lsum += p0 + p1;
-          pk[c] = pack_bf16(p0, p1);
+          for (int half = 0; half < 2; ++half) {
+            uint32_t pk[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              const int i = half * 64 + 2 * c;
+              const uint64_t x = ffma2(pack_f32x2(s[i], s[i + 1]), sl2x2, negm);
+              float x0, x1;
+              unpack_f32x2(x, x0, x1);
+              const float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
+              acc[c & 3] = fadd2(acc[c & 3], pack_f32x2(p0, p1));
+              pk[c] = pack_bf16(p0, p1);
+            }
+            DLLM_TMEM_ST32(tS + half * 32, pk);
+          }
+          float a0, a1, a2, a3, a4, a5, a6, a7;
+          unpack_f32x2(fadd2(acc[0], acc[1]), a0, a1);
+          unpack_f32x2(fadd2(acc[2], acc[3]), a2, a3);
+          (void)a4; (void)a5; (void)a6; (void)a7;
+          lsum += (a0 + a1) + (a2 + a3);
         }
-        DLLM_TMEM_ST32(tS + 0, (pk + 0));
-        DLLM_TMEM_ST32(tS + 32, (pk + 32));
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
