@@ -14,8 +14,12 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libdllm.so")
+TRACE = os.environ.get("DLLM_TRACE_BUILD") == "1"       # dev: timestamped refresh kernel
+VARIANT = os.environ.get("DLLM_VARIANT", "")              # dev: extra -D flags, e.g. "DLLM_POLY_PAIRS=2"
+_tag = ("_trace" if TRACE else "") + ("_" + VARIANT.replace("=", "").replace(",", "_") if VARIANT else "")
+BUILD = os.path.join(HERE, "_build" + _tag)
+LIB = os.path.join(HERE, f"libdllm{_tag}.so")
+EXTRA = (["-DDLLM_TRACE"] if TRACE else []) + [f"-D{v}" for v in VARIANT.split(",") if v]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
@@ -30,7 +34,7 @@ def _compile(src: str, verbose: bool) -> str:
     deps.append(os.path.join(HERE, "..", "include", "dllm.h"))
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", srcp, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, "-c", srcp, "-o", obj]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -83,6 +83,30 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   return d;
 }
 
+// 2^x for a pair on the FMA pipe (Cody-Waite split + degree-3 minimax polynomial
+// on [-0.5, 0.5], max relative error 7.8e-5 -- far below the bf16 rounding of P).
+// Offloads part of the softmax exponentials from the 16/clk/SM MUFU unit.
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
+  float x0, x1;
+  unpack_f32x2(x, x0, x1);
+  const uint64_t xc = pack_f32x2(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+  const uint64_t magic = pack_f32x2(12582912.f, 12582912.f);       // 1.5 * 2^23
+  const uint64_t t = fadd2(xc, magic);                               // round(x) in the low mantissa bits
+  const uint64_t jf = fadd2(t, pack_f32x2(-12582912.f, -12582912.f));
+  const uint64_t f = ffma2(jf, pack_f32x2(-1.f, -1.f), xc);         // x - round(x) in [-0.5, 0.5]
+  uint64_t p = ffma2(pack_f32x2(0.055088683807510905f, 0.055088683807510905f), f,
+                     pack_f32x2(0.24260405145947916f, 0.24260405145947916f));
+  p = ffma2(p, f, pack_f32x2(0.6932762416819607f, 0.6932762416819607f));
+  p = ffma2(p, f, pack_f32x2(0.9999289403695112f, 0.9999289403695112f));
+  float p0, p1, t0, t1;
+  unpack_f32x2(p, p0, p1);
+  unpack_f32x2(t, t0, t1);
+  // scale by 2^round(x): add round(x) to the exponent field (low bits of t carry it)
+  const float r0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  const float r1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+  return pack_f32x2(r0, r1);
+}
+
 // Row-major smem tile with rows of D bf16 (D/8 16-byte chunks) and an XOR
 // swizzle on the chunk index so that ldmatrix over 8 consecutive rows hits 8
 // different bank groups.  Byte offset of (row, chunk).

@@ -40,6 +40,19 @@
 #include "plan.h"
 #include "tc_ptx.cuh"
 
+#ifdef DLLM_TRACE
+__device__ long long g_trace[16][512];
+#define TRACE(kind, it)                                                    \
+  do {                                                                     \
+    if (blockIdx.x == 0 && (it) < 512) g_trace[kind][it] = clock64();      \
+  } while (0)
+extern "C" __attribute__((visibility("default"))) int dllm_trace_read(long long *host) {
+  return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace));
+}
+#else
+#define TRACE(kind, it)
+#endif
+
 namespace dllm {
 namespace {
 
@@ -47,6 +60,24 @@ constexpr int TBM = 128;            // query rows per tile
 constexpr int TBN = 128;            // keys per K/V tile
 constexpr int TC_THREADS = 384;
 constexpr float kRescaleLog2 = 8.0f;
+#ifndef DLLM_POLY_PAIRS
+#define DLLM_POLY_PAIRS 0
+#endif
+constexpr int kPolyPairs = DLLM_POLY_PAIRS;
+#ifndef DLLM_SPEC_MAX
+#define DLLM_SPEC_MAX 0
+#endif
+#ifndef DLLM_PINGPONG
+#define DLLM_PINGPONG 0
+#endif
+#ifndef DLLM_L2_PREFETCH
+#define DLLM_L2_PREFETCH 0
+#endif
+constexpr bool kSpecMax = DLLM_SPEC_MAX;     // exponentials with the running max, check afterwards
+constexpr bool kPingPong = DLLM_PINGPONG;    // strict MUFU turn-taking between the softmax warpgroups
+constexpr bool kL2Prefetch = DLLM_L2_PREFETCH;   // of every 8 column pairs, this many use the FMA-pipe exp2
+constexpr int kPrefetchLead = 4;     // K/V tiles before the end of a unit at which the next one is prefetched
+constexpr int kPrefetchTiles = 2;    // K/V tiles of the next unit prefetched into L2
 
 template <int D>
 struct TcCfg {
@@ -58,7 +89,8 @@ struct TcCfg {
   static constexpr int kOffV = kOffK + 2 * kKVBytes;     // 2 V stages
   static constexpr int kOffSc = kOffV + 2 * kKVBytes;    // [2 wg][2 buf][4 warps][128] f32
   static constexpr int kOffBar = kOffSc + 2 * 2 * 4 * 128 * 4;
-  static constexpr int kBytes = kOffBar + 256 + 1024;    // + 1024 alignment slack
+  static constexpr int kOffReq = kOffBar + 256;          // ReqInfo[nreq] copy of the plan
+  static constexpr int kBytes = kOffReq + kMaxReqPerLaunch * (int)sizeof(ReqInfo) + 1024;  // + alignment slack
 };
 
 // barrier slots (8 bytes each)
@@ -73,9 +105,10 @@ __host__ __device__ __forceinline__ int tc_regular_tiles(int L) { return (L + TB
 __host__ __device__ __forceinline__ bool tc_straddles(int bs, int be) { return (bs / TBM) != ((be - 1) / TBM); }
 
 struct Unit {
-  int r;          // index into plan.r
   int h, kvh;
   int L, bs, be;
+  int q_off, bt_row;
+  int64_t score_off;
   int n;          // K/V tiles
   int tile[2];    // tile ids (tile[1] = -1: single-tile unit)
   int origin[2];
@@ -83,10 +116,16 @@ struct Unit {
   bool scores_on[2];
 };
 
-__device__ __forceinline__ void decode_unit(const Plan &pl, int unit, Unit &u) {
-  u.r = plan_find(pl, unit);
-  const ReqInfo &R = pl.r[u.r];
+// unit -> (request, head, tile pair); `rs` is the shared-memory copy of the plan's requests
+__device__ __forceinline__ void decode_unit(const Plan &pl, const ReqInfo *rs, int unit, Unit &u) {
+  int lo = 0, hi = pl.nreq - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (rs[mid].unit_off <= unit) lo = mid; else hi = mid - 1;
+  }
+  const ReqInfo &R = rs[lo];
   u.L = R.L; u.bs = R.bs; u.be = R.be;
+  u.q_off = R.q_off; u.bt_row = R.bt_row; u.score_off = R.score_off;
   const int nreg = tc_regular_tiles(u.L);
   const bool extra = pl.with_scores && tc_straddles(u.bs, u.be);
   const int ntiles = nreg + (extra ? 1 : 0);
@@ -119,6 +158,8 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto bar = [&](int i) { return sb + C::kOffBar + 8u * (uint32_t)i; };
 
+  ReqInfo *rs = reinterpret_cast<ReqInfo *>(gb + C::kOffReq);
+  for (int i = threadIdx.x; i < plan.nreq; i += blockDim.x) rs[i] = plan.r[i];
   if (threadIdx.x == 0) {
     ptx::mbar_init(bar(B_QFULL), 1);
     ptx::mbar_init(bar(B_QEMPTY), 1);
@@ -157,9 +198,8 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
     const uint32_t boxbytes = (uint32_t)boxrows * 128u;
     for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x, ++ucnt) {
       Unit u;
-      decode_unit(plan, unit, u);
-      const ReqInfo &R = plan.r[u.r];
-      const int32_t *bt = plan.block_table + (int64_t)R.bt_row * plan.pages_per_req;
+      decode_unit(plan, rs, unit, u);
+      const int32_t *bt = plan.block_table + (int64_t)u.bt_row * plan.pages_per_req;
       if (lane == 0) {
         ptx::mbar_wait(bar(B_QEMPTY), (ucnt & 1) ^ 1);
         const int ntile = u.tile[1] >= 0 ? 2 : 1;
@@ -167,12 +207,39 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
         for (int i = 0; i < ntile; ++i)
           for (int c = 0; c < C::kChunks; ++c)
             ptx::tma_load_3d(sb + C::kOffQ + i * C::kQBytes + c * TBM * 128, &tm_q, bar(B_QFULL), c * 64, u.h,
-                             R.q_off + u.origin[i]);
+                             u.q_off + u.origin[i]);
       }
       for (int j = 0; j < u.n; ++j, ++it) {
         const int s = it & 1;
         const uint32_t ph = (it >> 1) & 1;
         const int key_end = min(TBN, u.L - j * TBN);      // valid keys in this tile
+        if (kL2Prefetch && j == (u.n > kPrefetchLead ? u.n - kPrefetchLead : 0)) {
+          // warm L2 with the next unit's Q tiles and first K/V tiles, so that the
+          // unit boundary does not wait a full HBM round trip (all SMs cross unit
+          // boundaries at about the same time)
+          const int nu = unit + gridDim.x;
+          if (nu < plan.total_units) {
+            Unit v;
+            decode_unit(plan, rs, nu, v);
+            const int nt = v.tile[1] >= 0 ? 2 : 1;
+            if (lane < nt * C::kChunks)
+              ptx::tma_prefetch_3d(&tm_q, (lane % C::kChunks) * 64, v.h, v.q_off + v.origin[lane / C::kChunks]);
+            const int32_t *btn = plan.block_table + (int64_t)v.bt_row * plan.pages_per_req;
+            const int ntl = min(v.n, kPrefetchTiles);
+            for (int e = lane; e < ntl * nsub; e += 32) {
+              const int key0 = (e / nsub) * TBN + (e % nsub) * boxrows;
+              if (key0 < v.L) {
+                const int page = __ldg(btn + (key0 >> plan.page_shift));
+                const int slot = key0 & (plan.page_size - 1);
+                for (int c = 0; c < C::kChunks; ++c) {
+                  ptx::tma_prefetch_4d(&tm_k, c * 64, slot, v.kvh, page);
+                  ptx::tma_prefetch_4d(&tm_v, c * 64, slot, v.kvh, page);
+                }
+              }
+            }
+          }
+          __syncwarp();
+        }
         if (lane == 0) {
           int nvalid = 0;
           for (int sbx = 0; sbx < nsub; ++sbx) nvalid += (sbx * boxrows < key_end);
@@ -225,7 +292,7 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
       int it = 0, ucnt = 0, vzc = 0, pc[2] = {0, 0};
       for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x, ++ucnt) {
         Unit u;
-        decode_unit(plan, unit, u);
+        decode_unit(plan, rs, unit, u);
         const bool two = u.tile[1] >= 0;
         auto qk = [&](int i, int stage) {
 #pragma unroll
@@ -263,25 +330,32 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
           const int s = (it + j) & 1;
           const bool has_next = j + 1 < u.n;
           const int sn = (it + j + 1) & 1;
+          TRACE(10, it + j);
           ptx::mbar_wait(bar(B_VFULL + s), ((it + j) >> 1) & 1);
           if (j == u.n - 1 && (u.L % TBN) != 0) {
             ptx::mbar_wait(bar(B_VZ), vzc & 1);
             ++vzc;
           }
-          if (has_next) ptx::mbar_wait(bar(B_KFULL + sn), ((it + j + 1) >> 1) & 1);
+          TRACE(11, it + j);
           ptx::tc_fence_after();
+          TRACE(6, pc[0]);
           ptx::mbar_wait(bar(B_PFULL + 0), pc[0] & 1);
+          TRACE(7, pc[0]);
           ++pc[0];
           ptx::tc_fence_after();
           pv(0, s, j > 0);
           if (!has_next) ptx::mma_commit(bar(B_OFULL + 0));
           if (has_next) {
+            ptx::mbar_wait(bar(B_KFULL + sn), ((it + j + 1) >> 1) & 1);
+            ptx::tc_fence_after();
             qk(0, sn);
             ptx::mma_commit(bar(B_SFULL + 0));
             if (!two && j + 1 == u.n - 1) ptx::mma_commit(bar(B_QEMPTY));
           }
           if (two) {
+            TRACE(8, pc[1]);
             ptx::mbar_wait(bar(B_PFULL + 1), pc[1] & 1);
+            TRACE(9, pc[1]);
             ++pc[1];
             ptx::tc_fence_after();
             pv(1, s, j > 0);
@@ -316,16 +390,17 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
     int sc = 0, oc = 0;
     for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x) {
       Unit u;
-      decode_unit(plan, unit, u);
-      if (u.tile[wg] < 0) continue;
-      const ReqInfo &R = plan.r[u.r];
-      const int origin = u.origin[wg];
-      const bool sc_on = u.scores_on[wg] && scores != nullptr;
+      decode_unit(plan, rs, unit, u);
+      if ((wg ? u.tile[1] : u.tile[0]) < 0) continue;
+      const int origin = (wg ? u.origin[1] : u.origin[0]);
+      const bool sc_on = (wg ? u.scores_on[1] : u.scores_on[0]) && scores != nullptr;
       const int rb0 = u.bs - origin, rb1 = u.be - origin;    // block rows within the tile
       const bool in_blk = sc_on && row >= rb0 && row < rb1;
       float m_used = -INFINITY, lsum = 0.f;
       for (int j = 0; j < u.n; ++j) {
+        if ((threadIdx.x & 127) == 0) TRACE(0 + wg, sc);
         ptx::mbar_wait(bar(B_SFULL + wg), sc & 1);
+        if ((threadIdx.x & 127) == 0) TRACE(2 + wg, sc);
         ++sc;
         ptx::tc_fence_after();
         uint32_t sr[128];
@@ -334,6 +409,7 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
         DLLM_TMEM_LD32(tS + 64, (sr + 64));
         DLLM_TMEM_LD32(tS + 96, (sr + 96));
         ptx::tmem_wait_ld();
+        if (threadIdx.x == 128) TRACE(12, sc - 1);
         float *s = reinterpret_cast<float *>(sr);
         if (sc_on) {
           float *buf = sbuf + (j & 1) * (4 * 128);
@@ -363,7 +439,7 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
           for (int w2 = 0; w2 < 4; ++w2)
             if ((w2 * 32 < rb1) && (w2 * 32 + 32 > rb0)) m = fmaxf(m, buf[w2 * 128 + row]);
           const int key = j * TBN + row;
-          if (key < u.L) scores[R.score_off + (int64_t)u.h * u.L + key] = m;
+          if (key < u.L) scores[u.score_off + (int64_t)u.h * u.L + key] = m;
         }
         if (j == u.n - 1) {
           const int key_end = u.L - j * TBN;
@@ -373,30 +449,33 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
               if (c >= key_end) s[c] = -INFINITY;
           }
         }
-        // row max: 8 independent 3-input max chains, then a tree
-        float mx;
-        {
+        // Softmax with a speculative (stale) max: P = exp2(s*tau*log2e - m_used) is
+        // computed with the running max of the previous tiles while the row max of
+        // this tile is reduced alongside on the ALU pipe; only if it exceeds m_used
+        // by more than 2^8 (rare after the first tile) is O rescaled and P redone
+        // from S (still intact in TMEM).  The first tile of a unit takes its max first.
+        auto rowmax = [&](const float *v) {
           float t[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) t[i] = fmax3(s[i], s[8 + i], s[16 + i]);
+          for (int i = 0; i < 8; ++i) t[i] = fmax3(v[i], v[8 + i], v[16 + i]);
 #pragma unroll
           for (int c = 24; c < 120; c += 16)
 #pragma unroll
-            for (int i = 0; i < 8; ++i) t[i] = fmax3(t[i], s[c + i], s[c + 8 + i]);
+            for (int i = 0; i < 8; ++i) t[i] = fmax3(t[i], v[c + i], v[c + 8 + i]);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) t[i] = fmaxf(t[i], s[120 + i]);
-          mx = fmax3(fmax3(t[0], t[1], t[2]), fmax3(t[3], t[4], t[5]), fmaxf(t[6], t[7]));
+          for (int i = 0; i < 8; ++i) t[i] = fmaxf(t[i], v[120 + i]);
+          return fmax3(fmax3(t[0], t[1], t[2]), fmax3(t[3], t[4], t[5]), fmaxf(t[6], t[7]));
+        };
+        // MUFU turn-taking: in a two-tile unit the warpgroups run their exponential
+        // passes strictly alternately (WG0 j, WG1 j, WG0 j+1, ...) so that each pass
+        // has the SM's 16 ex2/clk to itself while the tensor core works on the other tile
+        const bool pingpong = kPingPong && u.tile[1] >= 0;
+        if (pingpong) {
+          if (wg == 0 && j > 0) ptx::named_bar_sync(3, 256);
+          if (wg == 1) ptx::named_bar_sync(4, 256);
         }
-        mx *= sl2;
-        // lazy rescale; tcgen05.ld/st are warp-collective, so the decision is warp-uniform
-        const bool need = j > 0 && mx > m_used + kRescaleLog2;
-        if (j == 0) m_used = mx;
-        if (__any_sync(0xffffffffu, need)) {
-          const float alpha = need ? fast_exp2(m_used - mx) : 1.f;
-          if (need) {
-            lsum *= alpha;
-            m_used = mx;
-          }
+        if (threadIdx.x == 128) TRACE(13, sc - 1);
+        auto rescale_o = [&](float alpha) {
 #pragma unroll 1
           for (int c = 0; c < D; c += 32) {
             uint32_t o[32];
@@ -406,36 +485,97 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
             for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
             DLLM_TMEM_ST32(tO + c, o);
           }
+        };
+        if (!kSpecMax) {
+          // exact row max first, lazy rescale of O before the exponentials
+          const float mx = rowmax(s) * sl2;
+          if (j == 0) {
+            m_used = mx;
+          } else {
+            const bool need = mx > m_used + kRescaleLog2;
+            if (__any_sync(0xffffffffu, need)) {
+              const float alpha = need ? fast_exp2(m_used - mx) : 1.f;
+              if (need) {
+                lsum *= alpha;
+                m_used = mx;
+              }
+              rescale_o(alpha);
+            }
+          }
+        } else if (j == 0) {
+          m_used = rowmax(s) * sl2;
         }
-        // P = exp2(s * tau*log2e - m) in packed fp32x2 FMA + MUFU, bf16 pairs to TMEM
-        {
+        uint32_t pk[64];
+        float lpart, mxr;
+        auto exp_pass = [&](const float *v) {
           const uint64_t sl2x2 = pack_f32x2(sl2, sl2);
           const uint64_t negm = pack_f32x2(-m_used, -m_used);
           uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+          float tm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            uint32_t pk[32];
-#pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              const int i = half * 64 + 2 * c;
-              const uint64_t x = ffma2(pack_f32x2(s[i], s[i + 1]), sl2x2, negm);
+          for (int c = 0; c < 64; ++c) {
+            const int i = 2 * c;
+            tm[c & 3] = fmax3(tm[c & 3], v[i], v[i + 1]);
+            const uint64_t x = ffma2(pack_f32x2(v[i], v[i + 1]), sl2x2, negm);
+            float p0, p1;
+            if ((c & 7) < kPolyPairs) {
+              unpack_f32x2(exp2_poly2(x), p0, p1);          // FMA pipe
+            } else {
               float x0, x1;
               unpack_f32x2(x, x0, x1);
-              const float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
-              acc[c & 3] = fadd2(acc[c & 3], pack_f32x2(p0, p1));
-              pk[c] = pack_bf16(p0, p1);
+              p0 = fast_exp2(x0);                           // MUFU
+              p1 = fast_exp2(x1);
             }
-            DLLM_TMEM_ST32(tS + half * 32, pk);
+            acc[c & 3] = fadd2(acc[c & 3], pack_f32x2(p0, p1));
+            pk[c] = pack_bf16(p0, p1);
           }
-          float a0, a1, a2, a3, a4, a5, a6, a7;
+          float a0, a1, a2, a3;
           unpack_f32x2(fadd2(acc[0], acc[1]), a0, a1);
           unpack_f32x2(fadd2(acc[2], acc[3]), a2, a3);
-          (void)a4; (void)a5; (void)a6; (void)a7;
-          lsum += (a0 + a1) + (a2 + a3);
+          lpart = (a0 + a1) + (a2 + a3);
+          mxr = fmaxf(fmaxf(tm[0], tm[1]), fmaxf(tm[2], tm[3]));
+        };
+        exp_pass(s);
+        if (pingpong) {
+          if (wg == 0) ptx::named_bar_arrive(4, 256);
+          if (wg == 1 && j + 1 < u.n) ptx::named_bar_arrive(3, 256);
         }
+        if (threadIdx.x == 128) TRACE(14, sc - 1);
+        if (kSpecMax && j > 0) {
+          const float mx = mxr * sl2;
+          const bool need = mx > m_used + kRescaleLog2;
+          // tcgen05.ld/st are warp-collective: the slow path is taken warp-uniformly
+          if (__any_sync(0xffffffffu, need)) {
+            const float alpha = need ? fast_exp2(m_used - mx) : 1.f;
+            if (need) {
+              lsum *= alpha;
+              m_used = mx;
+            }
+            rescale_o(alpha);
+            uint32_t sr2[128];
+            DLLM_TMEM_LD32(tS + 0, (sr2 + 0));
+            DLLM_TMEM_LD32(tS + 32, (sr2 + 32));
+            DLLM_TMEM_LD32(tS + 64, (sr2 + 64));
+            DLLM_TMEM_LD32(tS + 96, (sr2 + 96));
+            ptx::tmem_wait_ld();
+            float *s2 = reinterpret_cast<float *>(sr2);
+            if (j == u.n - 1) {
+              const int key_end = u.L - j * TBN;
+#pragma unroll
+              for (int c = 0; c < 128; ++c)
+                if (c >= key_end) s2[c] = -INFINITY;
+            }
+            exp_pass(s2);
+          }
+        }
+        lsum += lpart;
+        DLLM_TMEM_ST32(tS + 0, (pk + 0));
+        DLLM_TMEM_ST32(tS + 32, (pk + 32));
         ptx::tmem_wait_st();
+        if (threadIdx.x == 128) TRACE(15, sc - 1);
         ptx::tc_fence_before();
         __syncwarp();
+        if ((threadIdx.x & 127) == 0) TRACE(4 + wg, sc - 1);
         if (lane == 0) ptx::mbar_arrive(bar(B_PFULL + wg));
       }
       // ---- epilogue: O / l -> bf16 -> global
@@ -444,8 +584,8 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
       ptx::tc_fence_after();
       const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
       const int grow = origin + row;
-      const bool wr = grow < u.write_end[wg];
-      __nv_bfloat16 *dst = out + (int64_t)(R.q_off + grow) * HD + (int64_t)u.h * D;
+      const bool wr = grow < (wg ? u.write_end[1] : u.write_end[0]);
+      __nv_bfloat16 *dst = out + (int64_t)(u.q_off + grow) * HD + (int64_t)u.h * D;
 #pragma unroll 1
       for (int c = 0; c < D; c += 32) {
         uint32_t o[32];

@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdllm.so")
+LIB_PATH = os.environ.get("DLLM_LIB") or os.path.join(_HERE, "libdllm.so")   # DLLM_LIB: dev builds only
 
 DLLM_OK = 0
 DLLM_ERR_INVALID_ARG = -1
