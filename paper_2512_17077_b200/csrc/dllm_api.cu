@@ -27,6 +27,8 @@ cudaError_t launch_reuse(const Plan &, const void *, const void *, const void *,
                          cudaStream_t);
 cudaError_t launch_refresh_mma(const Plan &, const void *, const void *, const void *, void *, float *,
                                cudaStream_t);
+cudaError_t launch_reuse_ws(const Plan &, const void *, const void *, const void *, const int32_t *, void *,
+                            cudaStream_t);
 int refresh_mma_units(int L, int bs, int be, int H, bool with_scores);
 bool refresh_tc_supported(int D);
 int refresh_tc_units(int L, int bs, int be, int H, bool with_scores);
@@ -183,6 +185,13 @@ int cuda_fail(cudaError_t e, const char *what) {
   return fail(DLLM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+int reuse_impl_env() {
+  // DLLM_REUSE_IMPL=v1 selects the one-CTA-per-unit kernel (A/B comparisons).
+  const char *s = getenv("DLLM_REUSE_IMPL");
+  if (s && !strcmp(s, "v1")) return 0;
+  return 1;
+}
+
 int refresh_impl_env() {
   // DLLM_REFRESH_IMPL=mma forces the mma.sync kernel (A/B comparisons).
   const char *s = getenv("DLLM_REFRESH_IMPL");
@@ -282,7 +291,8 @@ int dllm_reuse_sparse_attn(const dllm_problem *p, const void *q_blk, const void 
       const int blk = p->blk_end[b] - p->blk_start[b];
       return p->num_heads * ((blk + 31) / 32);
     });
-    cudaError_t e = launch_reuse(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream);
+    cudaError_t e = reuse_impl_env() ? launch_reuse_ws(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream)
+                                     : launch_reuse(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "reuse launch");
   }
   return ok();

@@ -1,0 +1,381 @@
+// Reuse sparse attention, persistent warp-specialised variant
+// (§2.3, Eq. 4; per-head key sets of §4.5).
+//
+// For request b, query head h and the active block's query rows q:
+//   O_b[q,h] = softmax_j(tau Q_blk[q,h].K[j,kv(h)]) V[j,kv(h)],  j in [bs,be) ++ idx(b,h)
+// with K/V gathered in place from the paged cache (no pack, no assembly copy).
+//
+// Reuse is HBM-bound (~30 FLOP/B), and a work unit (b, h, 32 query rows) is
+// short (C1: 280 keys = 143 KB), so a one-CTA-per-unit kernel spends most of
+// its time filling and draining its pipeline.  Here one CTA per SM streams
+// all of its units' 64-key chunks through ONE ring that never drains between
+// units.  Roles (192 threads):
+//   warp 4  translator: position -> physical cache row (block-table lookup)
+//           for every key of every chunk, NT chunks ahead, into a smem ring;
+//   warp 5  loader: Q rows of each unit + 16-byte cp.async row gathers of K
+//           and V into an NS-stage ring, completion signalled with
+//           cp.async.mbarrier.arrive.noinc;
+//   warps 0-3 consumers: mma.sync m16n8k16 (bf16 -> fp32) S = Q K^T and
+//           O += P V with a register online softmax; warp w owns rows
+//           16*(w&1)..+16 and keys 32*(w>>1)..+32 of each chunk; the two key
+//           halves are merged through shared memory at the end of a unit.
+// Units of the heads of one KV group are adjacent in the unit order so their
+// overlapping selections are served from L2.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "plan.h"
+#include "tc_ptx.cuh"
+
+namespace dllm {
+namespace {
+
+constexpr int kWsConsumers = 4;
+constexpr int kWsThreads = (kWsConsumers + 2) * 32;
+constexpr int kRows = 32;          // query rows per unit
+constexpr int kChunk = 64;         // keys per ring stage
+constexpr int kNT = 8;             // translation ring depth (chunks)
+
+template <int D>
+struct WsCfg {
+  static constexpr int kNS = D >= 128 ? 4 : 6;           // data ring stages
+  static constexpr int kKV = kChunk * D * 2;             // one K (or V) chunk
+  static constexpr int kQ = kRows * D * 2;
+  static constexpr int kXStride = D / 2 + 4;             // floats per lane record in the merge buffer
+  static constexpr int kOffK = 0;
+  static constexpr int kOffV = kOffK + kNS * kKV;
+  static constexpr int kOffQ = kOffV + kNS * kKV;        // 2 buffers
+  static constexpr int kOffOffs = kOffQ + 2 * kQ;        // [kNT][kChunk] int32
+  static constexpr int kOffX = kOffOffs + kNT * kChunk * 4;   // [2 rh][32][kXStride] f32
+  static constexpr int kOffBar = kOffX + 2 * 32 * kXStride * 4;
+  static constexpr int kBytes = kOffBar + 8 * (2 * kNS + 2 * kNT + 4) + 128;
+};
+
+struct RUnit {
+  int b, h, kvh, rg, blk, bs, nk, k, blk_off, bt_row;
+  int64_t idx_off;
+};
+
+__device__ __forceinline__ void decode(const Plan &pl, int unit, RUnit &u) {
+  u.b = plan_find(pl, unit);
+  const ReqInfo &R = pl.r[u.b];
+  u.blk = R.be - R.bs;
+  u.bs = R.bs;
+  const int ngroups = (u.blk + kRows - 1) / kRows;
+  const int local = unit - R.unit_off;
+  u.h = local / ngroups;
+  u.rg = local - u.h * ngroups;
+  u.kvh = u.h / (pl.H / pl.H_kv);
+  u.k = R.k;
+  u.nk = u.blk + R.k;
+  u.blk_off = R.blk_off;
+  u.bt_row = R.bt_row;
+  u.idx_off = R.idx_off + (int64_t)u.h * R.k;
+}
+
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(kWsThreads, 1)
+reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restrict__ q_blk,
+                const __nv_bfloat16 *__restrict__ k_cache, const __nv_bfloat16 *__restrict__ v_cache,
+                const int32_t *__restrict__ idx, __nv_bfloat16 *__restrict__ out) {
+  using C = WsCfg<D>;
+  constexpr int NS = C::kNS;
+  constexpr int CH = D / 8;
+  constexpr int KSTEPS = D / 16;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t sbase = smem_u32(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // barriers
+  const uint32_t b_full = sbase + C::kOffBar;                 // [NS] loader (32 noinc arrivals)
+  const uint32_t b_empty = b_full + 8 * NS;                   // [NS] consumers (4)
+  const uint32_t b_ofull = b_empty + 8 * NS;                  // [kNT] translator (1)
+  const uint32_t b_oempty = b_ofull + 8 * kNT;                // [kNT] loader (1)
+  const uint32_t b_qfull = b_oempty + 8 * kNT;                // [2] loader (32 noinc)
+  const uint32_t b_qempty = b_qfull + 16;                     // [2] consumers (4)
+  int32_t *offs = reinterpret_cast<int32_t *>(smem + C::kOffOffs);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      ptx::mbar_init(b_full + 8 * i, 32);
+      ptx::mbar_init(b_empty + 8 * i, kWsConsumers);
+    }
+    for (int i = 0; i < kNT; ++i) {
+      ptx::mbar_init(b_ofull + 8 * i, 1);
+      ptx::mbar_init(b_oempty + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(b_qfull + 8 * i, 32);
+      ptx::mbar_init(b_qempty + 8 * i, kWsConsumers);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kWsConsumers) {
+    // ============================ translator ============================
+    int t = 0;
+    for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x) {
+      RUnit u;
+      decode(plan, unit, u);
+      const int32_t *my_idx = idx + u.idx_off;
+      const int32_t *bt = plan.block_table + (int64_t)u.bt_row * plan.pages_per_req;
+      const int nchunks = (u.nk + kChunk - 1) / kChunk;
+      for (int c = 0; c < nchunks; ++c, ++t) {
+        const int slot = t % kNT;
+        ptx::mbar_wait(b_oempty + 8 * slot, ((t / kNT) & 1) ^ 1);
+#pragma unroll
+        for (int rr = 0; rr < kChunk / 32; ++rr) {
+          const int j = c * kChunk + rr * 32 + lane;
+          int off = -1;
+          if (j < u.nk) {
+            const int pos = j < u.blk ? u.bs + j : __ldg(my_idx + (j - u.blk));
+            const int page = __ldg(bt + (pos >> plan.page_shift));
+            off = (page * plan.H_kv + u.kvh) * plan.page_size + (pos & (plan.page_size - 1));
+          }
+          offs[slot * kChunk + rr * 32 + lane] = off;
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(b_ofull + 8 * slot);
+      }
+    }
+  } else if (warp == kWsConsumers + 1) {
+    // ============================ loader ============================
+    int t = 0, qc = 0;
+    for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x, ++qc) {
+      RUnit u;
+      decode(plan, unit, u);
+      const int row0 = u.rg * kRows;
+      {
+        const int qb = qc & 1;
+        ptx::mbar_wait(b_qempty + 8 * qb, ((qc >> 1) & 1) ^ 1);
+        uint8_t *sq = smem + C::kOffQ + qb * C::kQ;
+        const int64_t HD = (int64_t)plan.H * D;
+        for (int i = lane; i < kRows * CH; i += 32) {
+          const int r = i / CH, c = i - r * CH;
+          const bool ok = row0 + r < u.blk;
+          const __nv_bfloat16 *src = q_blk + (int64_t)(u.blk_off + (ok ? row0 + r : 0)) * HD + (int64_t)u.h * D + c * 8;
+          cp_async16(smem_u32(sq + swz<D>(r, c)), src, ok ? 16 : 0);
+        }
+        cp_async_mbar_arrive_noinc(b_qfull + 8 * qb);
+      }
+      const int nchunks = (u.nk + kChunk - 1) / kChunk;
+      for (int c = 0; c < nchunks; ++c, ++t) {
+        const int slot = t % kNT, s = t % NS;
+        ptx::mbar_wait(b_ofull + 8 * slot, (t / kNT) & 1);
+        ptx::mbar_wait(b_empty + 8 * s, ((t / NS) & 1) ^ 1);
+        uint8_t *dk = smem + C::kOffK + s * C::kKV;
+        uint8_t *dv = smem + C::kOffV + s * C::kKV;
+        // lanes sweep (row, 16-byte column) pairs: consecutive lanes read consecutive
+        // 16-byte pieces of the same 2D-byte row (coalesced per row)
+#pragma unroll 4
+        for (int e = lane; e < kChunk * CH; e += 32) {
+          const int r = e / CH, cc = e - r * CH;
+          const int off = offs[slot * kChunk + r];
+          const int64_t goff = (int64_t)(off < 0 ? 0 : off) * D + cc * 8;
+          const int nb = off < 0 ? 0 : 16;
+          cp_async16(smem_u32(dk + swz<D>(r, cc)), k_cache + goff, nb);
+          cp_async16(smem_u32(dv + swz<D>(r, cc)), v_cache + goff, nb);
+        }
+        cp_async_mbar_arrive_noinc(b_full + 8 * s);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(b_oempty + 8 * slot);
+      }
+    }
+    cp_async_wait<0>();
+  } else {
+    // ============================ consumers ============================
+    const int rh = warp & 1, kh = warp >> 1;
+    const float sl2 = plan.scale_log2;
+    const int64_t HD = (int64_t)plan.H * D;
+    float *xrec = reinterpret_cast<float *>(smem + C::kOffX) + (rh * 32 + lane) * C::kXStride;
+    int t = 0, qc = 0;
+    for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x, ++qc) {
+      RUnit u;
+      decode(plan, unit, u);
+      const int nchunks = (u.nk + kChunk - 1) / kChunk;
+      uint32_t qf[KSTEPS][4];
+      {
+        const int qb = qc & 1;
+        ptx::mbar_wait(b_qfull + 8 * qb, (qc >> 1) & 1);
+        const uint8_t *sq = smem + C::kOffQ + qb * C::kQ;
+#pragma unroll
+        for (int kk = 0; kk < KSTEPS; ++kk) {
+          const int r = rh * 16 + (lane & 15);
+          ldmatrix_x4(qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], smem_u32(sq + swz<D>(r, kk * 2 + (lane >> 4))));
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(b_qempty + 8 * qb);
+      }
+      float o[D / 8][4];
+#pragma unroll
+      for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
+
+      for (int c = 0; c < nchunks; ++c, ++t) {
+        const int s = t % NS;
+        ptx::mbar_wait(b_full + 8 * s, (t / NS) & 1);
+        const uint8_t *tk = smem + C::kOffK + s * C::kKV;
+        const uint8_t *tv = smem + C::kOffV + s * C::kKV;
+        float sc[4][4];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+#pragma unroll
+        for (int np = 0; np < 2; ++np) {
+#pragma unroll
+          for (int kk = 0; kk < KSTEPS; ++kk) {
+            const int key = kh * 32 + np * 16 + (lane >> 4) * 8 + (lane & 7);
+            const int cc = kk * 2 + ((lane >> 3) & 1);
+            uint32_t b0, b1, b2, b3;
+            ldmatrix_x4(b0, b1, b2, b3, smem_u32(tk + swz<D>(key, cc)));
+            mma_bf16_16816(sc[np * 2 + 0], qf[kk], b0, b1);
+            mma_bf16_16816(sc[np * 2 + 1], qf[kk], b2, b3);
+          }
+        }
+        const int kbase = c * kChunk + kh * 32 + (lane & 3) * 2;
+        float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int j = kbase + nt * 8 + (e & 1);
+            const float v = j < u.nk ? sc[nt][e] * sl2 : -INFINITY;
+            sc[nt][e] = v;
+            mx[e >> 1] = fmaxf(mx[e >> 1], v);
+          }
+        }
+        float alpha[2], mbase[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+          mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+          const float mnew = fmaxf(m_r[r], mx[r]);
+          mbase[r] = mnew == -INFINITY ? 0.f : mnew;
+          alpha[r] = fast_exp2(m_r[r] - mbase[r]);
+          m_r[r] = mnew;
+          l_r[r] *= alpha[r];
+        }
+#pragma unroll
+        for (int i = 0; i < D / 8; ++i) {
+          o[i][0] *= alpha[0]; o[i][1] *= alpha[0];
+          o[i][2] *= alpha[1]; o[i][3] *= alpha[1];
+        }
+        uint32_t pa[2][4];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const float p0 = fast_exp2(sc[nt][0] - mbase[0]);
+          const float p1 = fast_exp2(sc[nt][1] - mbase[0]);
+          const float p2 = fast_exp2(sc[nt][2] - mbase[1]);
+          const float p3 = fast_exp2(sc[nt][3] - mbase[1]);
+          const uint32_t lo = pack_bf16(p0, p1), hi = pack_bf16(p2, p3);
+          const __nv_bfloat162 blo = *reinterpret_cast<const __nv_bfloat162 *>(&lo);
+          const __nv_bfloat162 bhi = *reinterpret_cast<const __nv_bfloat162 *>(&hi);
+          l_r[0] += __low2float(blo) + __high2float(blo);
+          l_r[1] += __low2float(bhi) + __high2float(bhi);
+          pa[nt >> 1][(nt & 1) * 2 + 0] = lo;
+          pa[nt >> 1][(nt & 1) * 2 + 1] = hi;
+        }
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+#pragma unroll
+          for (int dp = 0; dp < D / 16; ++dp) {
+            const int key = kh * 32 + ks * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+            const int cc = dp * 2 + (lane >> 4);
+            uint32_t b0, b1, b2, b3;
+            ldmatrix_x4_trans(b0, b1, b2, b3, smem_u32(tv + swz<D>(key, cc)));
+            mma_bf16_16816(o[dp * 2 + 0], pa[ks], b0, b1);
+            mma_bf16_16816(o[dp * 2 + 1], pa[ks], b2, b3);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(b_empty + 8 * s);
+      }
+      // ---- merge the two key halves and store
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 1);
+        l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 2);
+      }
+      if (kh == 1) {
+#pragma unroll
+        for (int i = 0; i < D / 8; ++i)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) xrec[i * 4 + e] = o[i][e];
+        xrec[D / 2 + 0] = m_r[0]; xrec[D / 2 + 1] = m_r[1];
+        xrec[D / 2 + 2] = l_r[0]; xrec[D / 2 + 3] = l_r[1];
+      }
+      ptx::named_bar_sync(1, kWsConsumers * 32);
+      if (kh == 0) {
+        float sc_self[2], sc_other[2], inv[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const float m2 = xrec[D / 2 + r], l2 = xrec[D / 2 + 2 + r];
+          const float m = fmaxf(m_r[r], m2);
+          const float mb = m == -INFINITY ? 0.f : m;
+          sc_self[r] = fast_exp2(m_r[r] - mb);
+          sc_other[r] = fast_exp2(m2 - mb);
+          const float l = l_r[r] * sc_self[r] + l2 * sc_other[r];
+          inv[r] = l > 0.f ? 1.f / l : 0.f;
+        }
+        const int qr0 = u.rg * kRows + rh * 16 + (lane >> 2);
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int qrow = qr0 + r * 8;
+          if (qrow >= u.blk) continue;
+          __nv_bfloat16 *dst = out + (int64_t)(u.blk_off + qrow) * HD + (int64_t)u.h * D + (lane & 3) * 2;
+#pragma unroll
+          for (int i = 0; i < D / 8; ++i) {
+            const float v0 = (o[i][r * 2 + 0] * sc_self[r] + xrec[i * 4 + r * 2 + 0] * sc_other[r]) * inv[r];
+            const float v1 = (o[i][r * 2 + 1] * sc_self[r] + xrec[i * 4 + r * 2 + 1] * sc_other[r]) * inv[r];
+            *reinterpret_cast<uint32_t *>(dst + i * 8) = pack_bf16(v0, v1);
+          }
+        }
+      }
+      ptx::named_bar_sync(1, kWsConsumers * 32);      // merge buffer free for the next unit
+    }
+  }
+}
+
+int num_sms_ws() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int D>
+cudaError_t launch_ws_d(const Plan &plan, const void *q_blk, const void *k_cache, const void *v_cache,
+                        const int32_t *idx, void *out, cudaStream_t st) {
+  const int smem = WsCfg<D>::kBytes;
+  cudaError_t e = cudaFuncSetAttribute(reuse_ws_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int grid = plan.total_units < num_sms_ws() ? plan.total_units : num_sms_ws();
+  if (grid <= 0) return cudaSuccess;
+  reuse_ws_kernel<D><<<grid, kWsThreads, smem, st>>>(plan, (const __nv_bfloat16 *)q_blk,
+                                                     (const __nv_bfloat16 *)k_cache, (const __nv_bfloat16 *)v_cache,
+                                                     idx, (__nv_bfloat16 *)out);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_reuse_ws(const Plan &plan, const void *q_blk, const void *k_cache, const void *v_cache,
+                            const int32_t *idx, void *out, cudaStream_t st) {
+  switch (plan.D) {
+    case 16: return launch_ws_d<16>(plan, q_blk, k_cache, v_cache, idx, out, st);
+    case 32: return launch_ws_d<32>(plan, q_blk, k_cache, v_cache, idx, out, st);
+    case 64: return launch_ws_d<64>(plan, q_blk, k_cache, v_cache, idx, out, st);
+    case 128: return launch_ws_d<128>(plan, q_blk, k_cache, v_cache, idx, out, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dllm
