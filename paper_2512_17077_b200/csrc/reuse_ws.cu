@@ -32,15 +32,24 @@ namespace dllm {
 namespace {
 
 constexpr int kWsConsumers = 4;
-constexpr int kWsThreads = (kWsConsumers + 2) * 32;
+#ifndef DLLM_RWS_LOADERS
+#define DLLM_RWS_LOADERS 4
+#endif
+#ifndef DLLM_RWS_NS
+#define DLLM_RWS_NS 4
+#endif
+constexpr int kLoaders = DLLM_RWS_LOADERS;   // cp.async issuing warps
+constexpr int kWsThreads = (kWsConsumers + 1 + kLoaders) * 32;
 constexpr int kRows = 32;          // query rows per unit
 constexpr int kChunk = 64;         // keys per ring stage
 constexpr int kNT = 8;             // translation ring depth (chunks)
+constexpr int kTG = 8;             // chunks translated per batch
 
 template <int D>
 struct WsCfg {
-  static constexpr int kNS = D >= 128 ? 4 : 6;           // data ring stages
-  static constexpr int kKV = kChunk * D * 2;             // one K (or V) chunk
+  static constexpr int kNS = D >= 128 ? DLLM_RWS_NS : 6;  // data ring stages
+  static constexpr int kRowB = D * 2 + 16;               // padded smem row (conflict-free ldmatrix)
+  static constexpr int kKV = kChunk * kRowB;             // one K (or V) chunk
   static constexpr int kQ = kRows * D * 2;
   static constexpr int kXStride = D / 2 + 4;             // floats per lane record in the merge buffer
   static constexpr int kOffK = 0;
@@ -101,12 +110,12 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
-      ptx::mbar_init(b_full + 8 * i, 32);
+      ptx::mbar_init(b_full + 8 * i, 32 * kLoaders);
       ptx::mbar_init(b_empty + 8 * i, kWsConsumers);
     }
     for (int i = 0; i < kNT; ++i) {
       ptx::mbar_init(b_ofull + 8 * i, 1);
-      ptx::mbar_init(b_oempty + 8 * i, 1);
+      ptx::mbar_init(b_oempty + 8 * i, kLoaders);
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(b_qfull + 8 * i, 32);
@@ -125,32 +134,44 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
       const int32_t *my_idx = idx + u.idx_off;
       const int32_t *bt = plan.block_table + (int64_t)u.bt_row * plan.pages_per_req;
       const int nchunks = (u.nk + kChunk - 1) / kChunk;
-      for (int c = 0; c < nchunks; ++c, ++t) {
-        const int slot = t % kNT;
-        ptx::mbar_wait(b_oempty + 8 * slot, ((t / kNT) & 1) ^ 1);
+      // batches of kTG chunks: all index loads of a batch are issued together, then
+      // all block-table loads, so a batch costs two memory round trips, not 2 per chunk
+      for (int g0 = 0; g0 < nchunks; g0 += kTG) {
+        constexpr int Q = kTG * kChunk / 32;
+        int pos[Q], off[Q];
 #pragma unroll
-        for (int rr = 0; rr < kChunk / 32; ++rr) {
-          const int j = c * kChunk + rr * 32 + lane;
-          int off = -1;
-          if (j < u.nk) {
-            const int pos = j < u.blk ? u.bs + j : __ldg(my_idx + (j - u.blk));
-            const int page = __ldg(bt + (pos >> plan.page_shift));
-            off = (page * plan.H_kv + u.kvh) * plan.page_size + (pos & (plan.page_size - 1));
-          }
-          offs[slot * kChunk + rr * 32 + lane] = off;
+        for (int q = 0; q < Q; ++q) {
+          const int j = g0 * kChunk + q * 32 + lane;
+          pos[q] = j < u.nk ? (j < u.blk ? u.bs + j : __ldg(my_idx + (j - u.blk))) : -1;
         }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(b_ofull + 8 * slot);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int page = pos[q] >= 0 ? __ldg(bt + (pos[q] >> plan.page_shift)) : 0;
+          off[q] = pos[q] >= 0 ? (page * plan.H_kv + u.kvh) * plan.page_size + (pos[q] & (plan.page_size - 1)) : -1;
+        }
+        const int ng = min(kTG, nchunks - g0);
+#pragma unroll
+        for (int c = 0; c < kTG; ++c) {
+          if (c >= ng) break;
+          const int slot = t % kNT;
+          ptx::mbar_wait(b_oempty + 8 * slot, ((t / kNT) & 1) ^ 1);
+#pragma unroll
+          for (int rr = 0; rr < kChunk / 32; ++rr) offs[slot * kChunk + rr * 32 + lane] = off[c * (kChunk / 32) + rr];
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(b_ofull + 8 * slot);
+          ++t;
+        }
       }
     }
-  } else if (warp == kWsConsumers + 1) {
-    // ============================ loader ============================
+  } else if (warp > kWsConsumers) {
+    // ============================ loaders ============================
+    const int li = warp - kWsConsumers - 1;
     int t = 0, qc = 0;
     for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x, ++qc) {
       RUnit u;
       decode(plan, unit, u);
       const int row0 = u.rg * kRows;
-      {
+      if (li == 0) {
         const int qb = qc & 1;
         ptx::mbar_wait(b_qempty + 8 * qb, ((qc >> 1) & 1) ^ 1);
         uint8_t *sq = smem + C::kOffQ + qb * C::kQ;
@@ -170,16 +191,17 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
         ptx::mbar_wait(b_empty + 8 * s, ((t / NS) & 1) ^ 1);
         uint8_t *dk = smem + C::kOffK + s * C::kKV;
         uint8_t *dv = smem + C::kOffV + s * C::kKV;
-        // lanes sweep (row, 16-byte column) pairs: consecutive lanes read consecutive
-        // 16-byte pieces of the same 2D-byte row (coalesced per row)
+        // 16-byte cp.async row gathers: consecutive lanes read consecutive 16-byte pieces
+        // of the same 2D-byte row (coalesced per row); rows past the key list are
+        // zero-filled (src-size 0); completion counted with cp.async.mbarrier.arrive.noinc
 #pragma unroll 4
-        for (int e = lane; e < kChunk * CH; e += 32) {
+        for (int e = li * 32 + lane; e < kChunk * CH; e += 32 * kLoaders) {
           const int r = e / CH, cc = e - r * CH;
           const int off = offs[slot * kChunk + r];
           const int64_t goff = (int64_t)(off < 0 ? 0 : off) * D + cc * 8;
           const int nb = off < 0 ? 0 : 16;
-          cp_async16(smem_u32(dk + swz<D>(r, cc)), k_cache + goff, nb);
-          cp_async16(smem_u32(dv + swz<D>(r, cc)), v_cache + goff, nb);
+          cp_async16(smem_u32(dk + r * C::kRowB + cc * 16), k_cache + goff, nb);
+          cp_async16(smem_u32(dv + r * C::kRowB + cc * 16), v_cache + goff, nb);
         }
         cp_async_mbar_arrive_noinc(b_full + 8 * s);
         __syncwarp();
@@ -231,7 +253,7 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
             const int key = kh * 32 + np * 16 + (lane >> 4) * 8 + (lane & 7);
             const int cc = kk * 2 + ((lane >> 3) & 1);
             uint32_t b0, b1, b2, b3;
-            ldmatrix_x4(b0, b1, b2, b3, smem_u32(tk + swz<D>(key, cc)));
+            ldmatrix_x4(b0, b1, b2, b3, smem_u32(tk + key * C::kRowB + cc * 16));
             mma_bf16_16816(sc[np * 2 + 0], qf[kk], b0, b1);
             mma_bf16_16816(sc[np * 2 + 1], qf[kk], b2, b3);
           }
@@ -286,7 +308,7 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
             const int key = kh * 32 + ks * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
             const int cc = dp * 2 + (lane >> 4);
             uint32_t b0, b1, b2, b3;
-            ldmatrix_x4_trans(b0, b1, b2, b3, smem_u32(tv + swz<D>(key, cc)));
+            ldmatrix_x4_trans(b0, b1, b2, b3, smem_u32(tv + key * C::kRowB + cc * 16));
             mma_bf16_16816(o[dp * 2 + 0], pa[ks], b0, b1);
             mma_bf16_16816(o[dp * 2 + 1], pa[ks], b2, b3);
           }

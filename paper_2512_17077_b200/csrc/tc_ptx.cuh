@@ -62,6 +62,13 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const void *tmap, uint
       : "memory");
 }
 
+// 1-D bulk copy global -> shared (TMA engine), completion as tx bytes on `bar`
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
 // L2-only prefetch of a tensor-map box (no shared memory, no barrier)
 __device__ __forceinline__ void tma_prefetch_3d(const void *tmap, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(
