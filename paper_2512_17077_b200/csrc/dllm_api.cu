@@ -31,6 +31,9 @@ cudaError_t launch_reuse_ws(const Plan &, const void *, const void *, const void
                             cudaStream_t);
 int refresh_mma_units(int L, int bs, int be, int H, bool with_scores);
 bool refresh_tc_supported(int D);
+int refresh_tc2_units(int L, int bs, int be, int H, bool with_scores);
+cudaError_t launch_refresh_tc2(const Plan &, const void *, const void *, const void *, void *, float *,
+                               cudaStream_t);
 int refresh_tc_units(int L, int bs, int be, int H, bool with_scores);
 cudaError_t launch_refresh_tc(const Plan &, const void *, const void *, const void *, void *, float *,
                               cudaStream_t);
@@ -193,10 +196,12 @@ int reuse_impl_env() {
 }
 
 int refresh_impl_env() {
-  // DLLM_REFRESH_IMPL=mma forces the mma.sync kernel (A/B comparisons).
+  // DLLM_REFRESH_IMPL=mma | tc1 selects the mma.sync kernel or the single-buffered
+  // tcgen05 kernel (A/B comparisons); default: tcgen05 with double-buffered S (tc2).
   const char *s = getenv("DLLM_REFRESH_IMPL");
   if (s && !strcmp(s, "mma")) return 0;
-  return 1;
+  if (s && !strcmp(s, "tc1")) return 1;
+  return 2;
 }
 
 }  // namespace
@@ -235,18 +240,21 @@ int dllm_refresh_attn(const dllm_problem *p, const void *q, const void *k_cache,
     return fail(DLLM_ERR_SHAPE, "refresh: bf16 tensors must be 16-byte aligned");
   if (scores && ((uintptr_t)scores & 3u)) return fail(DLLM_ERR_SHAPE, "refresh: scores must be 4-byte aligned");
   const bool with_scores = scores != nullptr;
-  const bool use_tc = refresh_impl_env() && refresh_tc_supported(p->head_dim);
+  const int impl = refresh_tc_supported(p->head_dim) ? refresh_impl_env() : 0;
   cudaStream_t s = (cudaStream_t)stream;
   static thread_local Plan pl;
   for (int b0 = 0; b0 < B; b0 += kMaxReqPerLaunch) {
     const int b1 = b0 + kMaxReqPerLaunch < B ? b0 + kMaxReqPerLaunch : B;
     fill_plan(pl, p, lay.k, b0, b1, lay.cu_L, lay.cu_blk, lay.cu_k, [&](int b) {
-      return use_tc ? refresh_tc_units(p->seq_len[b], p->blk_start[b], p->blk_end[b], p->num_heads, with_scores)
-                    : refresh_mma_units(p->seq_len[b], p->blk_start[b], p->blk_end[b], p->num_heads, with_scores);
+      const int L = p->seq_len[b], bs = p->blk_start[b], be = p->blk_end[b], H = p->num_heads;
+      return impl == 2 ? refresh_tc2_units(L, bs, be, H, with_scores)
+             : impl == 1 ? refresh_tc_units(L, bs, be, H, with_scores)
+                         : refresh_mma_units(L, bs, be, H, with_scores);
     });
     pl.with_scores = with_scores;
-    cudaError_t e = use_tc ? launch_refresh_tc(pl, q, k_cache, v_cache, out, scores, s)
-                           : launch_refresh_mma(pl, q, k_cache, v_cache, out, scores, s);
+    cudaError_t e = impl == 2 ? launch_refresh_tc2(pl, q, k_cache, v_cache, out, scores, s)
+                    : impl == 1 ? launch_refresh_tc(pl, q, k_cache, v_cache, out, scores, s)
+                                : launch_refresh_mma(pl, q, k_cache, v_cache, out, scores, s);
     if (e != cudaSuccess) return cuda_fail(e, "refresh launch");
   }
   return ok();

@@ -1,0 +1,586 @@
+// Refresh dense attention on the 5th-generation tensor cores (sm_100a), with
+// double-buffered score tiles: Eq. 3 (§2.3) + the raw
+// per-head importance of Eq. 6 (inner term, §4.5).
+//
+// Why double buffering: when P_i(j) overwrites S_i(j) in TMEM (the P-aliases-S
+// trick), Q_i K_{j+1}^T cannot start before P_i(j) has been consumed, so every
+// softmax pass sits on the critical path of its own tile:
+//   period = softmax + (P.V + Q.K^T) + latencies.
+// Here K/V advance in 64-key steps and each 128-row Q tile owns TWO 64-column
+// score buffers (TMEM: S_i[0], S_i[1], O_i; 2 tiles x 256 columns = 512), so
+// Q_i K_{j+1}^T runs while the softmax works on S_i(j) and the softmax warps
+// go from one step to the next without waiting for the tensor core.
+//
+// Persistent, warp-specialised, one CTA per SM (384 threads):
+//   warp 8      TMA producer: Q tiles (3-D map over [sum L, H, D]) and 64-key
+//               K/V tiles straight out of the paged cache (4-D map over
+//               [pages, H_kv, P, D]) into 4-stage K and V rings (128-B swizzle).
+//   warp 9      MMA issuer (one thread) + TMEM owner:
+//               S_i(j) = Q_i K_j^T   (tcgen05.mma SS, M=128 N=64),
+//               O_i   += P_i(j) V_j  (tcgen05.mma TS, P from TMEM, M=128 N=D).
+//   warps 0-3   softmax warpgroup 0 (Q tile 0), one thread per query row;
+//   warps 4-7   softmax warpgroup 1 (Q tile 1): tcgen05.ld of S, online
+//               softmax in fp32 (log2 domain, lazy rescale: O is rescaled in
+//               TMEM only when the running max grows by more than 2^8, after
+//               waiting for the previous P.V), bf16 P back into the S buffer,
+//               final O / l and store.
+// Work unit = (request b, query head h, pair of 128-row Q tiles); the
+// importance epilogue and the extra "score tile" for blocks that straddle a
+// tile boundary are as in refresh_tc.cu.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "plan.h"
+#include "tc_ptx.cuh"
+
+#ifdef DLLM_TRACE
+__device__ long long g_trace2[16][512];
+#define TRACE2(kind, it)                                                   \
+  do {                                                                     \
+    if (blockIdx.x == 0 && (it) < 512) g_trace2[kind][it] = clock64();     \
+  } while (0)
+extern "C" __attribute__((visibility("default"))) int dllm_trace2_read(long long *host) {
+  return (int)cudaMemcpyFromSymbol(host, g_trace2, sizeof(g_trace2));
+}
+#else
+#define TRACE2(kind, it)
+#endif
+
+namespace dllm {
+namespace {
+
+constexpr int TBM = 128;            // query rows per tile
+constexpr int TBN = 64;             // keys per step
+constexpr int NST = 4;              // K and V ring stages
+constexpr int THREADS = 384;
+constexpr float kRescaleLog2 = 8.0f;
+
+template <int D>
+struct Cfg {
+  static constexpr int kChunks = D / 64;                 // 128-byte swizzle chunks per row
+  static constexpr int kQBytes = TBM * D * 2;
+  static constexpr int kKVBytes = TBN * D * 2;
+  static constexpr int kOffQ = 0;                        // 2 Q tiles
+  static constexpr int kOffK = 2 * kQBytes;              // NST K stages
+  static constexpr int kOffV = kOffK + NST * kKVBytes;   // NST V stages
+  static constexpr int kOffSc = kOffV + NST * kKVBytes;  // [2 wg][2 buf][4 warps][64] f32
+  static constexpr int kOffBar = kOffSc + 2 * 2 * 4 * TBN * 4;
+  static constexpr int kOffReq = kOffBar + 512;
+  static constexpr int kBytes = kOffReq + kMaxReqPerLaunch * (int)sizeof(ReqInfo) + 1024;
+};
+
+// barrier slots (8 bytes each)
+enum : int {
+  B_QFULL = 0, B_QEMPTY = 1,
+  B_KFULL = 2, B_KEMPTY = B_KFULL + NST, B_VFULL = B_KEMPTY + NST, B_VEMPTY = B_VFULL + NST,
+  B_VZ = B_VEMPTY + NST,
+  B_SFULL = B_VZ + 1,          // [tile][buf]
+  B_PFULL = B_SFULL + 4,       // [tile][buf]
+  B_ODONE = B_PFULL + 4,       // [tile][buf]: P.V of that buffer completed
+  B_OFULL = B_ODONE + 4,       // [tile]: last P.V of the unit completed
+  B_TMEMSLOT = B_OFULL + 2
+};
+__host__ __device__ constexpr uint32_t tmem_s(int tile, int buf) { return (uint32_t)(tile * 128 + buf * 64); }
+__host__ __device__ constexpr uint32_t tmem_o(int tile) { return tile ? 384u : 256u; }
+
+__host__ __device__ __forceinline__ int regular_tiles(int L) { return (L + TBM - 1) / TBM; }
+__host__ __device__ __forceinline__ bool straddles(int bs, int be) { return (bs / TBM) != ((be - 1) / TBM); }
+
+struct Unit {
+  int h, kvh;
+  int L, bs, be;
+  int q_off, bt_row;
+  int64_t score_off;
+  int n;          // 64-key steps
+  int tile1;      // 1 if the second Q tile exists
+  int origin0, origin1;
+  int wend0, wend1;
+  int sc0, sc1;   // importance epilogue on tile 0 / 1
+};
+
+__device__ __forceinline__ void decode_unit(const Plan &pl, const ReqInfo *rs, int unit, Unit &u) {
+  int lo = 0, hi = pl.nreq - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (rs[mid].unit_off <= unit) lo = mid; else hi = mid - 1;
+  }
+  const ReqInfo &R = rs[lo];
+  u.L = R.L; u.bs = R.bs; u.be = R.be;
+  u.q_off = R.q_off; u.bt_row = R.bt_row; u.score_off = R.score_off;
+  const int nreg = regular_tiles(u.L);
+  const bool extra = pl.with_scores && straddles(u.bs, u.be);
+  const int ntiles = nreg + (extra ? 1 : 0);
+  const int npairs = (ntiles + 1) >> 1;
+  const int local = unit - R.unit_off;
+  u.h = local / npairs;
+  const int p = local - u.h * npairs;
+  u.kvh = u.h / (pl.H / pl.H_kv);
+  u.n = (u.L + TBN - 1) / TBN;
+  const int t0 = 2 * p, t1 = 2 * p + 1;
+  u.tile1 = t1 < ntiles;
+  u.origin0 = t0 < nreg ? t0 * TBM : u.bs;
+  u.origin1 = t1 < nreg ? t1 * TBM : u.bs;
+  u.wend0 = t0 < nreg ? u.L : 0;
+  u.wend1 = t1 < nreg ? u.L : 0;
+  u.sc0 = pl.with_scores && (t0 == nreg || (!extra && t0 == u.bs / TBM));
+  u.sc1 = pl.with_scores && u.tile1 && (t1 == nreg || (!extra && t1 == u.bs / TBM));
+}
+
+template <int D>
+__global__ void __launch_bounds__(THREADS, 1)
+refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUtensorMap tm_q,
+                   const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                   __nv_bfloat16 *__restrict__ out, float *__restrict__ scores) {
+  using C = Cfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_u32 = smem_u32(smem_raw);
+  const uint32_t sb = (raw_u32 + 1023u) & ~1023u;
+  uint8_t *gb = smem_raw + (sb - raw_u32);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto bar = [&](int i) { return sb + C::kOffBar + 8u * (uint32_t)i; };
+
+  ReqInfo *rs = reinterpret_cast<ReqInfo *>(gb + C::kOffReq);
+  for (int i = threadIdx.x; i < plan.nreq; i += blockDim.x) rs[i] = plan.r[i];
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(bar(B_QFULL), 1);
+    ptx::mbar_init(bar(B_QEMPTY), 1);
+    for (int s = 0; s < NST; ++s) {
+      ptx::mbar_init(bar(B_KFULL + s), 1);
+      ptx::mbar_init(bar(B_KEMPTY + s), 1);
+      ptx::mbar_init(bar(B_VFULL + s), 1);
+      ptx::mbar_init(bar(B_VEMPTY + s), 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      ptx::mbar_init(bar(B_SFULL + i), 1);
+      ptx::mbar_init(bar(B_PFULL + i), 4);
+      ptx::mbar_init(bar(B_ODONE + i), 1);
+    }
+    ptx::mbar_init(bar(B_OFULL + 0), 1);
+    ptx::mbar_init(bar(B_OFULL + 1), 1);
+    ptx::mbar_init(bar(B_VZ), 1);
+    ptx::fence_mbar_init();
+    ptx::tma_prefetch_desc(&tm_q);
+    ptx::tma_prefetch_desc(&tm_k);
+    ptx::tma_prefetch_desc(&tm_v);
+  }
+  // roles: warps 0-7 softmax (two aligned warpgroups, TMEM lane quarter = warp % 4),
+  // warp 8 TMA producer, warp 9 MMA issuer.  The warp scheduler favours the highest
+  // warp id among eligible warps of a sub-partition, so the producer and the MMA
+  // issuer are placed above the softmax warps sharing their sub-partitions.
+  constexpr int kProducerWarp = 8, kMmaWarp = 9;
+  if (warp == kMmaWarp) {
+    ptx::tmem_alloc(bar(B_TMEMSLOT), 512);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t *>(gb + C::kOffBar + 8 * B_TMEMSLOT);
+
+  if (warp == kProducerWarp) {
+    // ============================ TMA producer ============================
+    int it = 0, ucnt = 0;
+    const int boxrows = plan.page_size < TBN ? plan.page_size : TBN;
+    const int nsub = TBN / boxrows;
+    const uint32_t boxbytes = (uint32_t)boxrows * 128u;
+    for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x, ++ucnt) {
+      Unit u;
+      decode_unit(plan, rs, unit, u);
+      const int32_t *bt = plan.block_table + (int64_t)u.bt_row * plan.pages_per_req;
+      if (lane == 0) {
+        ptx::mbar_wait(bar(B_QEMPTY), (ucnt & 1) ^ 1);
+        const int ntile = u.tile1 ? 2 : 1;
+        ptx::mbar_arrive_expect_tx(bar(B_QFULL), (uint32_t)(ntile * C::kQBytes));
+        for (int i = 0; i < ntile; ++i)
+          for (int c = 0; c < C::kChunks; ++c)
+            ptx::tma_load_3d(sb + C::kOffQ + i * C::kQBytes + c * TBM * 128, &tm_q, bar(B_QFULL), c * 64, u.h,
+                             u.q_off + (i ? u.origin1 : u.origin0));
+      }
+      for (int j = 0; j < u.n; ++j, ++it) {
+        const int s = it % NST;
+        const uint32_t ph = (it / NST) & 1;
+        const int key_end = min(TBN, u.L - j * TBN);      // valid keys in this step
+        if (lane == 0) {
+          int nvalid = 0;
+          for (int sbx = 0; sbx < nsub; ++sbx) nvalid += (sbx * boxrows < key_end);
+          const uint32_t bytes = (uint32_t)(nvalid * C::kChunks) * boxbytes;
+          ptx::mbar_wait(bar(B_KEMPTY + s), ph ^ 1);
+          ptx::mbar_arrive_expect_tx(bar(B_KFULL + s), bytes);
+          for (int sbx = 0; sbx < nvalid; ++sbx) {
+            const int key0 = j * TBN + sbx * boxrows;
+            const int page = __ldg(bt + (key0 >> plan.page_shift));
+            const int slot = key0 & (plan.page_size - 1);
+            for (int c = 0; c < C::kChunks; ++c)
+              ptx::tma_load_4d(sb + C::kOffK + s * C::kKVBytes + c * TBN * 128 + sbx * boxrows * 128, &tm_k,
+                               bar(B_KFULL + s), c * 64, slot, u.kvh, page);
+          }
+          ptx::mbar_wait(bar(B_VEMPTY + s), ph ^ 1);
+          ptx::mbar_arrive_expect_tx(bar(B_VFULL + s), bytes);
+          for (int sbx = 0; sbx < nvalid; ++sbx) {
+            const int key0 = j * TBN + sbx * boxrows;
+            const int page = __ldg(bt + (key0 >> plan.page_shift));
+            const int slot = key0 & (plan.page_size - 1);
+            for (int c = 0; c < C::kChunks; ++c)
+              ptx::tma_load_4d(sb + C::kOffV + s * C::kKVBytes + c * TBN * 128 + sbx * boxrows * 128, &tm_v,
+                               bar(B_VFULL + s), c * 64, slot, u.kvh, page);
+          }
+        }
+        __syncwarp();
+        if (key_end < TBN) {
+          // zero V rows >= key_end (P is 0 there, but 0 * NaN would poison O)
+          ptx::mbar_wait(bar(B_VFULL + s), ph);
+          uint8_t *vbase = gb + C::kOffV + s * C::kKVBytes;
+          const int nrow = TBN - key_end;
+          for (int e = lane; e < nrow * 8 * C::kChunks; e += 32) {
+            const int c = e / (nrow * 8);
+            const int rem = e - c * nrow * 8;
+            const int r = key_end + rem / 8;
+            *reinterpret_cast<uint4 *>(vbase + c * TBN * 128 + r * 128 + (rem & 7) * 16) = make_uint4(0, 0, 0, 0);
+          }
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(bar(B_VZ));
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ============================ MMA issuer ============================
+    // The whole warp runs this loop (warp-uniform control flow and descriptors,
+    // kept in uniform registers); one elected lane issues each tcgen05 op.
+    {
+      constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(TBM, TBN, false, false);
+      constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(TBM, D, false, true);
+      const uint64_t dq = ptx::smem_desc_sw128(sb + C::kOffQ, 16, 1024);
+      const uint64_t dk = ptx::smem_desc_sw128(sb + C::kOffK, 16, 1024);
+      const uint64_t dv = ptx::smem_desc_sw128(sb + C::kOffV, TBN * 128, 1024);
+      int it = 0, ucnt = 0, vzc = 0;
+      int gs[2] = {0, 0};        // S tiles issued per Q tile (buffer = gs & 1)
+      int gp[2] = {0, 0};        // P.V issued per Q tile
+      for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x, ++ucnt) {
+        Unit u;
+        decode_unit(plan, rs, unit, u);
+        const int nt = u.tile1 ? 2 : 1;
+        auto qk = [&](int i, int stage) {
+          const int b = gs[i] & 1;
+          const uint64_t a0 = dq + (uint64_t)((i * C::kQBytes) >> 4);
+          const uint64_t b0 = dk + (uint64_t)((stage * C::kKVBytes) >> 4);
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t ko = (uint32_t)(((k >> 2) * TBM * 128 + (k & 3) * 32) >> 4);
+            const uint32_t kb = (uint32_t)(((k >> 2) * TBN * 128 + (k & 3) * 32) >> 4);
+            ptx::mma_ss_elect(tmem + tmem_s(i, b), a0 + ko, b0 + kb, idesc_qk, k > 0);
+          }
+          ptx::mma_commit_elect(bar(B_SFULL + 2 * i + b));
+          ++gs[i];
+        };
+        auto pv = [&](int i, int stage, bool acc, bool last) {
+          const int b = gp[i] & 1;
+          const uint64_t v0 = dv + (uint64_t)((stage * C::kKVBytes) >> 4);
+#pragma unroll
+          for (int k = 0; k < TBN / 16; ++k)
+            ptx::mma_ts_elect(tmem + tmem_o(i), tmem + tmem_s(i, b) + (uint32_t)(k * 8), v0 + (uint64_t)((k * 16 * 128) >> 4),
+                              idesc_pv, (acc || k > 0) ? 1u : 0u);
+          ptx::mma_commit_elect(bar(B_ODONE + 2 * i + b));
+          if (last) ptx::mma_commit_elect(bar(B_OFULL + i));
+          ++gp[i];
+        };
+        ptx::mbar_wait(bar(B_QFULL), ucnt & 1);
+        ptx::tc_fence_after();
+        // prologue: S(0) and S(1) of every tile
+        const int npro = u.n < 2 ? u.n : 2;
+        for (int jj = 0; jj < npro; ++jj) {
+          const int st = (it + jj) % NST;
+          ptx::mbar_wait(bar(B_KFULL + st), ((it + jj) / NST) & 1);
+          ptx::tc_fence_after();
+          for (int i = 0; i < nt; ++i) qk(i, st);
+          ptx::mma_commit_elect(bar(B_KEMPTY + st));
+        }
+        if (u.n <= 2) ptx::mma_commit_elect(bar(B_QEMPTY));
+        for (int j = 0; j < u.n; ++j) {
+          const int sv = (it + j) % NST;
+          if (lane == 0) TRACE2(10, it + j);
+          ptx::mbar_wait(bar(B_VFULL + sv), ((it + j) / NST) & 1);
+          if (lane == 0) TRACE2(11, it + j);
+          if (j == u.n - 1 && (u.L % TBN) != 0) {
+            ptx::mbar_wait(bar(B_VZ), vzc & 1);
+            ++vzc;
+          }
+          const bool ahead = j + 2 < u.n;
+          const int sk = (it + j + 2) % NST;
+          for (int i = 0; i < nt; ++i) {
+            const int b = gp[i] & 1;
+            if (lane == 0) TRACE2(6 + 2 * i, gp[i]);
+            ptx::mbar_wait(bar(B_PFULL + 2 * i + b), (gp[i] >> 1) & 1);
+            if (lane == 0) TRACE2(7 + 2 * i, gp[i]);
+            ptx::tc_fence_after();
+            pv(i, sv, j > 0, j == u.n - 1);
+            if (ahead) {
+              if (i == 0) {
+                if (lane == 0) TRACE2(12, it + j);
+                ptx::mbar_wait(bar(B_KFULL + sk), ((it + j + 2) / NST) & 1);
+                if (lane == 0) TRACE2(13, it + j);
+                ptx::tc_fence_after();
+              }
+              qk(i, sk);
+            }
+          }
+          if (ahead) {
+            ptx::mma_commit_elect(bar(B_KEMPTY + sk));
+            if (j + 2 == u.n - 1) ptx::mma_commit_elect(bar(B_QEMPTY));
+          }
+          ptx::mma_commit_elect(bar(B_VEMPTY + sv));
+        }
+        it += u.n;
+      }
+    }
+    __syncwarp();
+  } else if (warp < 8) {
+    // ============================ softmax warpgroups ============================
+    const int wg = warp >> 2;
+    const int wq = warp & 3;                       // TMEM lane quarter
+    const int row = wq * 32 + lane;                // row of the Q tile == TMEM lane
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const uint32_t tO = tmem + lane_off + tmem_o(wg);
+    float *sbuf = reinterpret_cast<float *>(gb + C::kOffSc) + wg * (2 * 4 * TBN);
+    const float sl2 = plan.scale_log2;
+    const int64_t HD = (int64_t)plan.H * D;
+    int sc = 0, oc = 0;
+    for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x) {
+      Unit u;
+      decode_unit(plan, rs, unit, u);
+      if (wg == 1 && !u.tile1) continue;
+      const int origin = wg ? u.origin1 : u.origin0;
+      const bool sc_on = (wg ? u.sc1 : u.sc0) && scores != nullptr;
+      const int rb0 = u.bs - origin, rb1 = u.be - origin;    // block rows within the tile
+      const bool in_blk = sc_on && row >= rb0 && row < rb1;
+      const bool warp_blk = sc_on && (wq * 32 < rb1) && (wq * 32 + 32 > rb0);
+      float m_used = -INFINITY, lsum = 0.f;
+      for (int j = 0; j < u.n; ++j, ++sc) {
+        const int b = sc & 1;
+        const uint32_t tS = tmem + lane_off + tmem_s(wg, b);
+        if ((threadIdx.x & 127) == 0) TRACE2(0 + wg, sc);
+        ptx::mbar_wait(bar(B_SFULL + 2 * wg + b), (sc >> 1) & 1);
+        if ((threadIdx.x & 127) == 0) TRACE2(2 + wg, sc);
+        ptx::tc_fence_after();
+        uint32_t sr[64];
+        DLLM_TMEM_LD32(tS + 0, (sr + 0));
+        DLLM_TMEM_LD32(tS + 32, (sr + 32));
+        ptx::tmem_wait_ld();
+        float *s = reinterpret_cast<float *>(sr);
+        if (sc_on) {
+          // importance: column max of the UNSCALED S over the block rows
+          float *buf = sbuf + (j & 1) * (4 * TBN);
+          if (warp_blk) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              float v[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = in_blk ? s[c * 32 + i] : -INFINITY;
+#pragma unroll
+              for (int o = 16; o >= 1; o >>= 1) {
+                const bool up = (lane & o) != 0;
+#pragma unroll
+                for (int i = 0; i < o; ++i) {
+                  const float send = up ? v[i] : v[i + o];
+                  const float keep = up ? v[i + o] : v[i];
+                  v[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, o));
+                }
+              }
+              buf[wq * TBN + c * 32 + lane] = v[0];
+            }
+          }
+          ptx::named_bar_sync(1 + wg, 128);
+          if (row < TBN) {
+            float m = -INFINITY;
+#pragma unroll
+            for (int w2 = 0; w2 < 4; ++w2)
+              if ((w2 * 32 < rb1) && (w2 * 32 + 32 > rb0)) m = fmaxf(m, buf[w2 * TBN + row]);
+            const int key = j * TBN + row;
+            if (key < u.L) scores[u.score_off + (int64_t)u.h * u.L + key] = m;
+          }
+        }
+        if (j == u.n - 1) {
+          const int key_end = u.L - j * TBN;
+          if (key_end < TBN) {
+#pragma unroll
+            for (int c = 0; c < TBN; ++c)
+              if (c >= key_end) s[c] = -INFINITY;
+          }
+        }
+        float mx;
+        {
+          float t[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) t[i] = fmax3(s[i], s[8 + i], s[16 + i]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) t[i] = fmax3(t[i], s[24 + i], s[32 + i]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) t[i] = fmax3(t[i], s[40 + i], s[48 + i]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) t[i] = fmaxf(t[i], s[56 + i]);
+          mx = fmax3(fmax3(t[0], t[1], t[2]), fmax3(t[3], t[4], t[5]), fmaxf(t[6], t[7])) * sl2;
+        }
+        if (j == 0) {
+          m_used = mx;
+        } else {
+          // lazy rescale (warp-uniform: tcgen05.ld/st are warp-collective); O must
+          // hold P(j-1).V first, so wait for that P.V to complete
+          const bool need = mx > m_used + kRescaleLog2;
+          if (__any_sync(0xffffffffu, need)) {
+            const int pb = (sc - 1) & 1;
+            ptx::mbar_wait(bar(B_ODONE + 2 * wg + pb), ((sc - 1) >> 1) & 1);
+            ptx::tc_fence_after();
+            const float alpha = need ? fast_exp2(m_used - mx) : 1.f;
+            if (need) {
+              lsum *= alpha;
+              m_used = mx;
+            }
+#pragma unroll 1
+            for (int c = 0; c < D; c += 32) {
+              uint32_t o[32];
+              DLLM_TMEM_LD32(tO + c, o);
+              ptx::tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              DLLM_TMEM_ST32(tO + c, o);
+            }
+          }
+        }
+        {
+          const uint64_t sl2x2 = pack_f32x2(sl2, sl2);
+          const uint64_t negm = pack_f32x2(-m_used, -m_used);
+          uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+          uint32_t pk[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const uint64_t x = ffma2(pack_f32x2(s[2 * c], s[2 * c + 1]), sl2x2, negm);
+            float x0, x1;
+            unpack_f32x2(x, x0, x1);
+            const float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
+            acc[c & 3] = fadd2(acc[c & 3], pack_f32x2(p0, p1));
+            pk[c] = pack_bf16(p0, p1);
+          }
+          DLLM_TMEM_ST32(tS, pk);
+          float a0, a1, a2, a3;
+          unpack_f32x2(fadd2(acc[0], acc[1]), a0, a1);
+          unpack_f32x2(fadd2(acc[2], acc[3]), a2, a3);
+          lsum += (a0 + a1) + (a2 + a3);
+        }
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if ((threadIdx.x & 127) == 0) TRACE2(4 + wg, sc);
+        if (lane == 0) ptx::mbar_arrive(bar(B_PFULL + 2 * wg + b));
+      }
+      // ---- epilogue: O / l -> bf16 -> global
+      ptx::mbar_wait(bar(B_OFULL + wg), oc & 1);
+      ++oc;
+      ptx::tc_fence_after();
+      const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+      const int grow = origin + row;
+      const bool wr = grow < (wg ? u.wend1 : u.wend0);
+      __nv_bfloat16 *dst = out + (int64_t)(u.q_off + grow) * HD + (int64_t)u.h * D;
+#pragma unroll 1
+      for (int c = 0; c < D; c += 32) {
+        uint32_t o[32];
+        DLLM_TMEM_LD32(tO + c, o);
+        ptx::tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          pk[i] = pack_bf16(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
+        if (wr) {
+          uint4 *d4 = reinterpret_cast<uint4 *>(dst + c);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) d4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        }
+      }
+      ptx::tc_fence_before();
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == kMmaWarp) ptx::tmem_dealloc(tmem, 512);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+int num_sms() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+template <int D>
+cudaError_t launch_d(const Plan &plan, const void *q, const void *k, const void *v, void *out, float *scores,
+                     cudaStream_t st) {
+  auto enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  int64_t rows = 0;
+  for (int b = 0; b < plan.nreq; ++b) rows = rows > plan.r[b].q_off + plan.r[b].L ? rows : plan.r[b].q_off + plan.r[b].L;
+  CUtensorMap tq, tk, tv;
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)plan.H, (cuuint64_t)rows};
+    cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)plan.H * D * 2};
+    cuuint32_t box[3] = {64, 1, TBM};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(q), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {
+    const int P = plan.page_size;
+    cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)P, (cuuint64_t)plan.H_kv, (cuuint64_t)1 << 24};
+    cuuint64_t strides[3] = {(cuuint64_t)D * 2, (cuuint64_t)P * D * 2, (cuuint64_t)plan.H_kv * P * D * 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)(P < TBN ? P : TBN), 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    for (int w = 0; w < 2; ++w) {
+      if (enc(w ? &tv : &tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(w ? v : k), dims, strides, box,
+              es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    }
+  }
+  const int smem = Cfg<D>::kBytes;
+  cudaError_t e = cudaFuncSetAttribute(refresh_tc2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int grid = plan.total_units < num_sms() ? plan.total_units : num_sms();
+  if (grid <= 0) return cudaSuccess;
+  refresh_tc2_kernel<D><<<grid, THREADS, smem, st>>>(plan, tq, tk, tv, (__nv_bfloat16 *)out, scores);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int refresh_tc2_units(int L, int bs, int be, int H, bool with_scores) {
+  const int nt = regular_tiles(L) + ((with_scores && straddles(bs, be)) ? 1 : 0);
+  return H * ((nt + 1) / 2);
+}
+
+cudaError_t launch_refresh_tc2(const Plan &plan, const void *q, const void *k, const void *v, void *out,
+                               float *scores, cudaStream_t st) {
+  switch (plan.D) {
+    case 64: return launch_d<64>(plan, q, k, v, out, scores, st);
+    case 128: return launch_d<128>(plan, q, k, v, out, scores, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dllm
