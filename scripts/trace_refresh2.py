@@ -17,7 +17,7 @@ buf = lib.alloc_buffers(p)
 for _ in range(3):
     lib.refresh_attn(p, q, kc, vc, buf.out, buf.scores)
 torch.cuda.synchronize()
-tr = np.zeros((16, 512), dtype=np.int64)
+tr = np.zeros((24, 512), dtype=np.int64)
 lib.lib().dllm_trace2_read(tr.ctypes.data_as(ctypes.c_void_p))
 t0 = tr[0, 0]
 names = ["s0wait", "s1wait", "s0gotS", "s1gotS", "s0P", "s1P", "mWaitP0", "mGotP0", "mWaitP1", "mGotP1",
@@ -31,3 +31,30 @@ print("softmax1 S->P:", np.median(tr[5, :N] - tr[3, :N]), " wait S:", np.median(
 print("mma waitP0", np.median(tr[7, :N] - tr[6, :N]), "waitP1", np.median(tr[9, :N] - tr[8, :N]),
       "waitV", np.median(tr[11, :N] - tr[10, :N]), "waitK", np.median(tr[13, :N] - tr[12, :N]))
 print("period (sm0 gotS):", np.median(np.diff(tr[2, :N])))
+n_unit = (wl.seq_len[0] + 63) // 64
+g = np.diff(tr[2, :N])
+inner = [g[i] for i in range(len(g)) if (i + 1) % n_unit != 0]
+bound = [g[i] for i in range(len(g)) if (i + 1) % n_unit == 0]
+print(f"steps/unit {n_unit}: median inner period {np.median(inner):.0f}, median boundary gap {np.median(bound):.0f}, "
+      f"boundary overhead per unit {np.median(bound) - np.median(inner):.0f} clk = "
+      f"{(np.median(bound) - np.median(inner)) / (n_unit * np.median(inner)) * 100:.1f}% of a unit")
+# unit boundary anatomy (softmax WG0): last P of unit u -> O_full wait start/end -> epilogue end -> first S of u+1
+for u_ in range(1, 4):
+    lastP = tr[4, u_ * n_unit - 1]; ow0 = tr[14, 2 * (u_ - 1)]; ow1 = tr[14, 2 * (u_ - 1) + 1]
+    ep_end = tr[14, 256 + u_]; firstS = tr[2, u_ * n_unit]; firstS_wait = tr[0, u_ * n_unit]
+    print(f"unit {u_-1}->{u_}: lastP->Ofull wait done {ow1 - lastP}, epilogue {ep_end - ow1}, "
+          f"epilogue end->next S ready {firstS - ep_end}; MMA: last PV0 issue {tr[7, u_*n_unit-1]-lastP} after lastP, "
+          f"first V wait of next unit at {tr[10, u_*n_unit] - lastP}, got {tr[11, u_*n_unit] - lastP}")
+
+for u_ in range(1, 4):
+    lastP = tr[4, u_ * n_unit - 1]
+    print(f"unit {u_}: producer q_empty wait {tr[20,u_]-lastP}..{tr[21,u_]-lastP}; MMA Q wait {tr[16,u_]-lastP}..{tr[17,u_]-lastP}; "
+          f"K0 at {tr[18,u_]-lastP}, K1 at {tr[19,u_]-lastP} (relative to last P of unit {u_-1})")
+print("rows around the first boundary (absolute, minus t0):")
+print("iter " + " ".join(f"{n:>8s}" for n in names))
+for i in range(n_unit - 3, n_unit + 3):
+    print(f"{i:4d} " + " ".join(f"{(tr[k, i] - t0):8d}" for k in range(14)))
+print("WG1 epilogue O-wait", tr[15, 0] - t0, tr[15, 1] - t0, "end", tr[15, 257] - t0)
+print("WG0 epilogue O-wait", tr[14, 0] - t0, tr[14, 1] - t0, "end", tr[14, 257] - t0)
+print("MMA unit1 Qwait", tr[16, 1] - t0, tr[17, 1] - t0, "K0", tr[18, 1] - t0, "K1", tr[19, 1] - t0)
+print("MMA end of unit0 (after last commit)", tr[22, 0] - t0, " unit1 decode start/end", tr[23, 2] - t0, tr[23, 3] - t0)
