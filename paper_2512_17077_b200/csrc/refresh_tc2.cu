@@ -43,8 +43,17 @@ __device__ long long g_trace2[24][512];
   do {                                                                     \
     if (blockIdx.x == 0 && (it) < 512) g_trace2[kind][it] = clock64();     \
   } while (0)
+__device__ long long g_cta2[1024][4];
 extern "C" __attribute__((visibility("default"))) int dllm_trace2_read(long long *host) {
   return (int)cudaMemcpyFromSymbol(host, g_trace2, sizeof(g_trace2));
+}
+extern "C" __attribute__((visibility("default"))) int dllm_trace2_cta(long long *host) {
+  return (int)cudaMemcpyFromSymbol(host, g_cta2, sizeof(g_cta2));
+}
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 #else
 #define TRACE2(kind, it)
@@ -56,7 +65,7 @@ namespace {
 constexpr int TBM = 128;            // query rows per tile
 constexpr int TBN = 64;             // keys per step
 constexpr int NST = 4;              // K and V ring stages
-constexpr int THREADS = 384;
+constexpr int THREADS = 512;
 constexpr float kRescaleLog2 = 8.0f;
 #ifndef DLLM_TC2_PREFETCH
 #define DLLM_TC2_PREFETCH 0
@@ -78,8 +87,9 @@ struct Cfg {
   static constexpr int kOffV = kOffK + NST * kKVBytes;   // NST V stages
   static constexpr int kOffSc = kOffV + NST * kKVBytes;  // [2 wg][2 buf][4 warps][64] f32
   static constexpr int kOffBar = kOffSc + 2 * 2 * 4 * TBN * 4;
-  static constexpr int kOffStage = kOffBar + 1024;       // [8 warps][32 rows][64 B] epilogue staging (SW64)
-  static constexpr int kOffReq = kOffStage + 8 * 32 * 64;
+  static constexpr int kOffStage = kOffBar + 1024;       // [4 epilogue warps][32 rows][64 B] staging (SW64)
+  static constexpr int kOffL = kOffStage + 4 * 32 * 64;  // [2 parity][2 tiles][128] f32 row sums
+  static constexpr int kOffReq = kOffL + 2 * 2 * 128 * 4;
   // + nreq * sizeof(ReqInfo) + 1024 alignment slack, sized per launch
   static int bytes(int nreq) { return kOffReq + nreq * (int)sizeof(ReqInfo) + 1024; }
 };
@@ -93,7 +103,9 @@ enum : int {
   B_PFULL = B_SFULL + 4,       // [tile][buf]
   B_ODONE = B_PFULL + 4,       // [tile][buf]: P.V of that buffer completed
   B_OFULL = B_ODONE + 4,       // [tile]: last P.V of the unit completed
-  B_TMEMSLOT = B_OFULL + 2
+  B_OFREE = B_OFULL + 2,       // [tile]: epilogue has read O out of TMEM
+  B_LFULL = B_OFREE + 2,       // [tile]: softmax row sums of the unit in smem
+  B_TMEMSLOT = B_LFULL + 2
 };
 __host__ __device__ constexpr uint32_t tmem_s(int tile, int buf) { return (uint32_t)(tile * 128 + buf * 64); }
 __host__ __device__ constexpr uint32_t tmem_o(int tile) { return tile ? 384u : 256u; }
@@ -128,7 +140,11 @@ __device__ __forceinline__ void decode_unit(const Plan &pl, const ReqInfo *rs, i
   const int npairs = (ntiles + 1) >> 1;
   const int local = unit - R.unit_off;
   u.h = local / npairs;
-  const int p = local - u.h * npairs;
+  // tile pairs are rotated by head: units are dealt to CTAs with a stride of
+  // gridDim.x (a multiple of 4 on B200), so without the rotation one CTA in
+  // npairs would always get the pair that holds the active block, and with it
+  // all of the importance-epilogue work (a 30% longer critical path)
+  const int p = (local - u.h * npairs + u.h) % npairs;
   u.kvh = u.h / (pl.H / pl.H_kv);
   u.n = (u.L + TBN - 1) / TBN;
   const int t0 = 2 * p, t1 = 2 * p + 1;
@@ -155,6 +171,9 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto bar = [&](int i) { return sb + C::kOffBar + 8u * (uint32_t)i; };
 
+#ifdef DLLM_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 1024) { g_cta2[blockIdx.x][0] = gtimer(); g_cta2[blockIdx.x][2] = 0; }
+#endif
   ReqInfo *rs = reinterpret_cast<ReqInfo *>(gb + C::kOffReq);
   for (int i = threadIdx.x; i < plan.nreq; i += blockDim.x) rs[i] = plan.r[i];
   if (threadIdx.x == 0) {
@@ -171,8 +190,11 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
       ptx::mbar_init(bar(B_PFULL + i), 4);
       ptx::mbar_init(bar(B_ODONE + i), 1);
     }
-    ptx::mbar_init(bar(B_OFULL + 0), 1);
-    ptx::mbar_init(bar(B_OFULL + 1), 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(bar(B_OFULL + i), 1);
+      ptx::mbar_init(bar(B_OFREE + i), 4);
+      ptx::mbar_init(bar(B_LFULL + i), 4);
+    }
     ptx::mbar_init(bar(B_VZ), 1);
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&tm_q);
@@ -195,6 +217,7 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
 
   if (warp == kProducerWarp) {
     // ============================ TMA producer ============================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
     int it = 0, ucnt = 0;
     const int boxrows = plan.page_size < TBN ? plan.page_size : TBN;
     const int nsub = TBN / boxrows;
@@ -284,6 +307,7 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
     }
   } else if (warp == kQWarp) {
     // ============================ Q producer ============================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
     // (separate from the K/V producer so that the next unit's first K/V steps are
     // not queued behind the wait for the Q buffers to drain)
     if (lane == 0) {
@@ -308,6 +332,7 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
     __syncwarp();
   } else if (warp == kMmaWarp) {
     // ============================ MMA issuer ============================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
     // The whole warp runs this loop (warp-uniform control flow and descriptors,
     // kept in uniform registers); one elected lane issues each tcgen05 op.
     {
@@ -319,6 +344,7 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
       int it = 0, ucnt = 0, vzc = 0;
       int gs[2] = {0, 0};        // S tiles issued per Q tile (buffer = gs & 1)
       int gp[2] = {0, 0};        // P.V issued per Q tile
+      int ou[2] = {0, 0};        // units per Q tile (O accumulator reuse)
       Unit un;
       if (blockIdx.x < plan.total_units) decode_unit(plan, rs, blockIdx.x, un);
       for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x, ++ucnt) {
@@ -383,6 +409,11 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
             if (lane == 0) TRACE2(6 + 2 * i, gp[i]);
             ptx::mbar_wait(bar(B_PFULL + 2 * i + b), (gp[i] >> 1) & 1);
             if (lane == 0) TRACE2(7 + 2 * i, gp[i]);
+            if (j == 0) {
+              // the epilogue warpgroup must have read the previous unit's O_i
+              ptx::mbar_wait(bar(B_OFREE + i), (ou[i] & 1) ^ 1);
+              ++ou[i];
+            }
             ptx::tc_fence_after();
             pv(i, sv, j > 0, j == u.n - 1);
             if (ahead) {
@@ -408,6 +439,7 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
     __syncwarp();
   } else if (warp < 8) {
     // ============================ softmax warpgroups ============================
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 136;\n" ::: "memory");
     const int wg = warp >> 2;
     const int wq = warp & 3;                       // TMEM lane quarter
     const int row = wq * 32 + lane;                // row of the Q tile == TMEM lane
@@ -544,62 +576,93 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
         if ((threadIdx.x & 127) == 0) TRACE2(4 + wg, sc);
         if (lane == 0) ptx::mbar_arrive(bar(B_PFULL + 2 * wg + b));
       }
-      // ---- epilogue: O / l -> bf16 -> global
-      if ((threadIdx.x & 127) == 0) TRACE2(14 + wg, 2 * oc);
-      ptx::mbar_wait(bar(B_OFULL + wg), oc & 1);
-      if ((threadIdx.x & 127) == 0) TRACE2(14 + wg, 2 * oc + 1);
+      // ---- hand the row sums to the epilogue warpgroup (double-buffered by unit parity)
+      float *lb = reinterpret_cast<float *>(gb + C::kOffL) + ((oc & 1) * 2 + wg) * 128;
+      lb[row] = lsum;
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(bar(B_LFULL + wg));
       ++oc;
-      ptx::tc_fence_after();
-      const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
-      // O leaves through the TMA store engine: each warp stages 32 rows x 32 columns
-      // (64 B, 64-byte swizzle) in shared memory and one lane issues an asynchronous
-      // bulk tensor store, so the softmax warps do not wait for the HBM writes (all
-      // CTAs reach unit boundaries together).  Warps whose rows run past the end of
-      // the request (or of a score-only tile) store their valid rows directly.
-      uint8_t *stg = gb + C::kOffStage + warp * 32 * 64;
-      const uint32_t stg_s = sb + C::kOffStage + warp * 32 * 64;
-      const int wend = wg ? u.wend1 : u.wend0;
-      const int srow0 = origin + wq * 32;                  // first tile row of this warp
-      const bool full_warp = srow0 + 32 <= wend;
-#pragma unroll 1
-      for (int c = 0; c < D; c += 32) {
-        uint32_t o[32];
-        DLLM_TMEM_LD32(tO + c, o);
+    }
+  } else if (warp >= 12) {
+    // ============================ epilogue warpgroup ============================
+    // Reads O_i out of TMEM as soon as the unit's last P.V completes, releases the
+    // accumulator to the MMA warp, then normalises by the row sums and streams O to
+    // global through the TMA store engine.  The softmax warps never wait for it.
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 176;\n" ::: "memory");
+    const int wq = warp & 3;
+    const int row = wq * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const int64_t HD = (int64_t)plan.H * D;
+    uint8_t *stg = gb + C::kOffStage + wq * 32 * 64;
+    const uint32_t stg_s = sb + C::kOffStage + wq * 32 * 64;
+    int oc[2] = {0, 0};
+    for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x) {
+      Unit u;
+      decode_unit(plan, rs, unit, u);
+      for (int i = 0; i < (u.tile1 ? 2 : 1); ++i) {
+        const uint32_t tO = tmem + lane_off + tmem_o(i);
+        ptx::mbar_wait(bar(B_OFULL + i), oc[i] & 1);
+        ptx::tc_fence_after();
+        uint32_t o[D];
+#pragma unroll
+        for (int c = 0; c < D; c += 32) DLLM_TMEM_LD32(tO + c, (o + c));
         ptx::tmem_wait_ld();
-        uint32_t pk[16];
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(bar(B_OFREE + i));
+        ptx::mbar_wait(bar(B_LFULL + i), oc[i] & 1);
+        const float lsum = reinterpret_cast<const float *>(gb + C::kOffL)[((oc[i] & 1) * 2 + i) * 128 + row];
+        ++oc[i];
+        const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+        const int origin = i ? u.origin1 : u.origin0;
+        const int wend = i ? u.wend1 : u.wend0;
+        const int srow0 = origin + wq * 32;                // first tile row of this warp
+        const bool full_warp = srow0 + 32 <= wend;
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          pk[i] = pack_bf16(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
-        if (full_warp) {
-          if (lane == 0) ptx::bulk_wait_group_read0();     // previous chunk read out of staging
-          __syncwarp();
+        for (int c = 0; c < D; c += 32) {
+          uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int chunk = i ^ ((lane >> 1) & 3);          // 64-byte swizzle
-            *reinterpret_cast<uint4 *>(stg + lane * 64 + chunk * 16) =
-                make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          for (int e = 0; e < 16; ++e)
+            pk[e] = pack_bf16(__uint_as_float(o[c + 2 * e]) * inv, __uint_as_float(o[c + 2 * e + 1]) * inv);
+          if (full_warp) {
+            if (lane == 0) ptx::bulk_wait_group_read0();   // previous chunk read out of staging
+            __syncwarp();
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const int chunk = q4 ^ ((lane >> 1) & 3);      // 64-byte swizzle
+              *reinterpret_cast<uint4 *>(stg + lane * 64 + chunk * 16) =
+                  make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+            }
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              ptx::tma_store_3d(&tm_o, stg_s, c, u.h, u.q_off + srow0);
+              ptx::bulk_commit_group();
+            }
+          } else if (srow0 + lane < wend) {
+            uint4 *d4 = reinterpret_cast<uint4 *>(out + (int64_t)(u.q_off + srow0 + lane) * HD + (int64_t)u.h * D + c);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) d4[q4] = make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
           }
-          ptx::fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            ptx::tma_store_3d(&tm_o, stg_s, c, u.h, u.q_off + srow0);
-            ptx::bulk_commit_group();
-          }
-        } else if (srow0 + lane < wend) {
-          uint4 *d4 = reinterpret_cast<uint4 *>(out + (int64_t)(u.q_off + srow0 + lane) * HD + (int64_t)u.h * D + c);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) d4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
         }
       }
-      ptx::tc_fence_before();
-      if ((threadIdx.x & 127) == 0) TRACE2(14 + wg, 256 + oc);
     }
+    if (lane == 0) ptx::bulk_wait_group0();
+  } else if (warp >= 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
   }
 
-  if (warp < 8 && lane == 0) ptx::bulk_wait_group0();
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
+#ifdef DLLM_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 1024) {
+    g_cta2[blockIdx.x][1] = gtimer();
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_cta2[blockIdx.x][3] = smid;
+  }
+#endif
   if (warp == kMmaWarp) ptx::tmem_dealloc(tmem, 512);
 }
 

@@ -58,3 +58,15 @@ print("WG1 epilogue O-wait", tr[15, 0] - t0, tr[15, 1] - t0, "end", tr[15, 257] 
 print("WG0 epilogue O-wait", tr[14, 0] - t0, tr[14, 1] - t0, "end", tr[14, 257] - t0)
 print("MMA unit1 Qwait", tr[16, 1] - t0, tr[17, 1] - t0, "K0", tr[18, 1] - t0, "K1", tr[19, 1] - t0)
 print("MMA end of unit0 (after last commit)", tr[22, 0] - t0, " unit1 decode start/end", tr[23, 2] - t0, tr[23, 3] - t0)
+
+ct = np.zeros((1024, 4), dtype=np.int64)
+lib.lib().dllm_trace2_cta(ct.ctypes.data_as(ctypes.c_void_p))
+g = ct[:148]
+start = g[:, 0] - g[:, 0].min(); dur = g[:, 1] - g[:, 0]
+print(f"CTA start spread {start.max()/1e3:.1f} us; duration min/med/max {dur.min()/1e3:.1f}/{np.median(dur)/1e3:.1f}/{dur.max()/1e3:.1f} us; "
+      f"kernel span {(g[:,1].max()-g[:,0].min())/1e3:.1f} us")
+order = np.argsort(-dur)
+print("slowest CTAs (cta, smid, us):", [(int(c), int(g[c, 3]), round(dur[c] / 1e3, 1)) for c in order[:12]])
+print("fastest CTAs:", [(int(c), int(g[c, 3]), round(dur[c] / 1e3, 1)) for c in order[-6:]])
+hist = np.histogram(dur / 1e3, bins=10)
+print("hist", [int(x) for x in hist[0]], [round(float(x), 0) for x in hist[1]])
