@@ -126,14 +126,31 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
   __syncthreads();
 
   if (warp == kWsConsumers) {
-    // ============================ translator ============================
-    int t = 0;
+    // ============================ translator (+ Q rows) ============================
+    int t = 0, qc = 0;
     for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x) {
       RUnit u;
       decode(plan, unit, u);
       const int32_t *my_idx = idx + u.idx_off;
       const int32_t *bt = plan.block_table + (int64_t)u.bt_row * plan.pages_per_req;
       const int nchunks = (u.nk + kChunk - 1) / kChunk;
+      {
+        // the unit's query rows (the translator runs ahead of the loaders, so Q of
+        // the next unit is in flight long before the consumers need it)
+        const int row0 = u.rg * kRows;
+        const int qb = qc & 1;
+        ptx::mbar_wait(b_qempty + 8 * qb, ((qc >> 1) & 1) ^ 1);
+        uint8_t *sq = smem + C::kOffQ + qb * C::kQ;
+        const int64_t HD = (int64_t)plan.H * D;
+        for (int i = lane; i < kRows * CH; i += 32) {
+          const int r = i / CH, c = i - r * CH;
+          const bool ok = row0 + r < u.blk;
+          const __nv_bfloat16 *src = q_blk + (int64_t)(u.blk_off + (ok ? row0 + r : 0)) * HD + (int64_t)u.h * D + c * 8;
+          cp_async16(smem_u32(sq + swz<D>(r, c)), src, ok ? 16 : 0);
+        }
+        cp_async_mbar_arrive_noinc(b_qfull + 8 * qb);
+        ++qc;
+      }
       // batches of kTG chunks: all index loads of a batch are issued together, then
       // all block-table loads, so a batch costs two memory round trips, not 2 per chunk
       for (int g0 = 0; g0 < nchunks; g0 += kTG) {
@@ -163,27 +180,14 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
         }
       }
     }
+    cp_async_wait<0>();
   } else if (warp > kWsConsumers) {
     // ============================ loaders ============================
     const int li = warp - kWsConsumers - 1;
-    int t = 0, qc = 0;
-    for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x, ++qc) {
+    int t = 0;
+    for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x) {
       RUnit u;
       decode(plan, unit, u);
-      const int row0 = u.rg * kRows;
-      if (li == 0) {
-        const int qb = qc & 1;
-        ptx::mbar_wait(b_qempty + 8 * qb, ((qc >> 1) & 1) ^ 1);
-        uint8_t *sq = smem + C::kOffQ + qb * C::kQ;
-        const int64_t HD = (int64_t)plan.H * D;
-        for (int i = lane; i < kRows * CH; i += 32) {
-          const int r = i / CH, c = i - r * CH;
-          const bool ok = row0 + r < u.blk;
-          const __nv_bfloat16 *src = q_blk + (int64_t)(u.blk_off + (ok ? row0 + r : 0)) * HD + (int64_t)u.h * D + c * 8;
-          cp_async16(smem_u32(sq + swz<D>(r, c)), src, ok ? 16 : 0);
-        }
-        cp_async_mbar_arrive_noinc(b_qfull + 8 * qb);
-      }
       const int nchunks = (u.nk + kChunk - 1) / kChunk;
       for (int c = 0; c < nchunks; ++c, ++t) {
         const int slot = t % kNT, s = t % NS;
