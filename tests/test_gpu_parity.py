@@ -45,6 +45,11 @@ EDGE = {
     "r1_dense": custom("e_r1", [192], [96], [128], H=2, Hk=2, D=128, r=1.0),
     "tiny_r_w5": custom("e_tiny", [333], [300], [332], H=3, Hk=1, D=64, r=0.001, w=5),
     "w1": custom("e_w1", [129], [64], [96], H=2, Hk=2, D=128, w=1),
+    "p16_d128": custom("e_p16", [300, 77], [250, 40], [282, 72], H=4, Hk=2, D=128, P=16),
+    "p1024_d64": custom("e_p1024", [1500], [1400], [1432], H=2, Hk=1, D=64, P=1024),
+    "long_8k": custom("e_long", [8192], [8000], [8032], H=2, Hk=1, D=128, r=0.1),
+    "gqa_mixed_lengths": custom("e_gqamix", [640, 129, 1025, 64], [608, 0, 993, 32], [640, 32, 1025, 64],
+                                H=6, Hk=2, D=128),
 }
 
 
@@ -294,11 +299,13 @@ def test_check_indices(L):
 
 
 # ------------------------------------------------------------------ full-size configs, sampled outputs
-@pytest.mark.parametrize("cfg,sample", [("C1", [0, 9, 15]), ("C2", [0, 31])])
-def test_full_config_hot_path_sampled(L, cfg, sample):
+@pytest.mark.parametrize("cfg,sample,r,n", [("C1", [0, 9, 15], None, None), ("C2", [0, 31], None, None),
+                                           ("C3", [0, 77, 255], None, None), ("C4", [0, 7], 0.05, 8),
+                                           ("C4", [3], 1.0, 4)])
+def test_full_config_hot_path_sampled(L, cfg, sample, r, n):
     """BASELINE sizes, the launch configuration bench.py times: whole batch on the
     GPU, oracle on sampled requests (exact-integer Q/K so the selection is bit-exact)."""
-    wl = synth.config(cfg, kind="exact")
+    wl = synth.config(cfg, kind="exact", keep_ratio=r, num_requests=n)
     batch = synth.make_batch(wl)
     p = problem_of(batch)
     q, q_blk, kc, vc = to_dev(batch)
