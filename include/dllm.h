@@ -115,6 +115,14 @@ DLLM_API int dllm_refresh_attn(const dllm_problem *p, const void *q, const void 
  * Scores must be finite.  scores, idx: DEVICE. */
 DLLM_API int dllm_select_heads(const dllm_problem *p, const float *scores, int32_t *idx, void *stream);
 
+/* Uniform selection, the Sparse-dLLM baseline (§2.4, Eq. 5):
+ * S[c] = sum_h (pooled scores of head h)[c], summed in fp32 in ascending head
+ * order; ONE top-k set per request (same pooling, tie rule and order as
+ * dllm_select_heads), written to every head's slot of the idx layout so that
+ * dllm_reuse_sparse_attn runs the uniform baseline unchanged.  Bit-exact when
+ * the head sums are exact in fp32.  scores, idx: DEVICE. */
+DLLM_API int dllm_select_global(const dllm_problem *p, const float *scores, int32_t *idx, void *stream);
+
 /* Reuse (Eq. 4): out_blk[q, h] = softmax_j(tau * Qb[q,h].K[j,kv(h)]) . V[j,kv(h)]
  * over J^h = [bs, be) ++ idx(b, h), K/V read in place through the block table
  * (no pack, no copy).  The caller has written the active block's K/V rows

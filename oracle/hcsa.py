@@ -46,6 +46,7 @@ __all__ = [
     "attention_masked_dense",
     "refresh_batch",
     "select_batch",
+    "select_global_batch",
     "reuse_batch",
 ]
 
@@ -373,6 +374,23 @@ def select_batch(scores, seq_len, blk_start, blk_end, keep_ratio: float, window:
             out.append(np.zeros((sc.shape[0], 0), np.int64))
             continue
         out.append(C[select_topk(pool_scores(sc[:, C], window), k)])
+    return out
+
+
+def select_global_batch(scores, seq_len, blk_start, blk_end, keep_ratio: float, window: int):
+    """Uniform (Sparse-dLLM) selection from precomputed raw scores [H, L_b]:
+    S_j = sum_h pool(raw_h)[j] (§2.4, Eq. 5), one top-k per
+    request with the same tie rule and order (R6, R7).  Returns a
+    list of [k_b] int64 position arrays."""
+    out = []
+    for b, sc in enumerate(scores):
+        C = candidates(seq_len[b], blk_start[b], blk_end[b])
+        k = keep_count(keep_ratio, len(C))
+        if k == 0:
+            out.append(np.zeros((0,), np.int64))
+            continue
+        S = pool_scores(_f64(sc)[:, C], window).sum(axis=0)
+        out.append(C[select_topk(S, k)])
     return out
 
 

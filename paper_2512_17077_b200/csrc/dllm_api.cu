@@ -23,6 +23,7 @@
 namespace dllm {
 cudaError_t launch_select(const Plan &, const float *, int32_t *, cudaStream_t);
 cudaError_t launch_check_indices(const Plan &, const int32_t *, int32_t *, cudaStream_t);
+cudaError_t launch_select_global(const Plan &, const float *, int32_t *, cudaStream_t);
 cudaError_t launch_reuse(const Plan &, const void *, const void *, const void *, const int32_t *, void *,
                          cudaStream_t);
 cudaError_t launch_refresh_mma(const Plan &, const void *, const void *, const void *, void *, float *,
@@ -277,6 +278,27 @@ int dllm_select_heads(const dllm_problem *p, const float *scores, int32_t *idx, 
     if (pl.total_units == 0) continue;
     cudaError_t e = launch_select(pl, scores, idx, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "select launch");
+  }
+  return ok();
+}
+
+int dllm_select_global(const dllm_problem *p, const float *scores, int32_t *idx, void *stream) {
+  Layout lay;
+  int st = make_layout(p, lay);
+  if (st) return st;
+  const int B = p->num_requests;
+  if (B == 0) return ok();
+  if (!scores || !idx) return fail(DLLM_ERR_INVALID_ARG, "select_global: NULL pointer");
+  for (int b = 0; b < B; ++b)
+    if (p->seq_len[b] > DLLM_MAX_SELECT_LEN)
+      return fail(DLLM_ERR_UNSUPPORTED, "select_global: request %d seq_len=%d > %d", b, p->seq_len[b],
+                  DLLM_MAX_SELECT_LEN);
+  static thread_local Plan pl;
+  for (int b0 = 0; b0 < B; b0 += kMaxReqPerLaunch) {
+    const int b1 = b0 + kMaxReqPerLaunch < B ? b0 + kMaxReqPerLaunch : B;
+    fill_plan(pl, p, lay.k, b0, b1, lay.cu_L, lay.cu_blk, lay.cu_k, [&](int) { return 1; });
+    cudaError_t e = launch_select_global(pl, scores, idx, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "select_global launch");
   }
   return ok();
 }

@@ -160,6 +160,104 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
   }
 }
 
+// Uniform (global) selection, the Sparse-dLLM baseline of PAPER.md:136-145
+// (§2.4, Eq. 5): S[c] = sum over heads (ascending h, fp32) of the per-head pooled
+// score, one top-k per request with the same radix select / tie rule, and the
+// shared index set is written to EVERY head's slot of the idx layout so that
+// dllm_reuse_sparse_attn consumes it unchanged.  One CTA per request.
+__global__ void __launch_bounds__(kSelThreads)
+select_global_kernel(const __grid_constant__ Plan plan, const float *__restrict__ scores,
+                     int32_t *__restrict__ idx) {
+  extern __shared__ uint32_t keys[];                  // [n_ctx]
+  __shared__ int hist[256];
+  __shared__ int warp_buf[32];
+  __shared__ uint32_t s_prefix;
+  __shared__ int s_krem;
+  const ReqInfo &R = plan.r[blockIdx.x];
+  const int L = R.L, bs = R.bs, blk = R.be - R.bs;
+  const int n = L - blk;
+  const int k = R.k;
+  if (k <= 0) return;
+  const int H = plan.H;
+  const float *raw0 = scores + R.score_off;
+  const int half = plan.window >> 1;
+  for (int c = threadIdx.x; c < n; c += kSelThreads) {
+    const int lo = max(0, c - half), hi = min(n - 1, c + half);
+    float acc = 0.f;
+    for (int h = 0; h < H; ++h) {
+      const float *raw = raw0 + (int64_t)h * L;
+      float m = -INFINITY;
+      for (int j = lo; j <= hi; ++j) m = fmaxf(m, __ldg(raw + (j < bs ? j : j + blk)));
+      acc += m;
+    }
+    keys[c] = order_key(acc);
+  }
+  if (threadIdx.x == 0) { s_prefix = 0u; s_krem = k; }
+  __syncthreads();
+  uint32_t prefix = 0u, mask = 0u;
+  int krem = k;
+#pragma unroll 1
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += kSelThreads) hist[i] = 0;
+    __syncthreads();
+    for (int c = threadIdx.x; c < n; c += kSelThreads) {
+      const uint32_t key = keys[c];
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 0xffu], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      const int base = 8 * (31 - lane);
+      int cnt[8], sum = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { cnt[i] = hist[base + 7 - i]; sum += cnt[i]; }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int above = incl - sum;
+      if (above < krem && krem <= incl) {
+        int acc = above;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (acc + cnt[i] >= krem) {
+            s_prefix = prefix | ((uint32_t)(base + 7 - i) << shift);
+            s_krem = krem - acc;
+            break;
+          }
+          acc += cnt[i];
+        }
+      }
+    }
+    __syncthreads();
+    prefix = s_prefix;
+    krem = s_krem;
+    mask |= 0xffu << shift;
+    __syncthreads();
+  }
+  int eq_base = 0, out_base = 0;
+  int32_t *out0 = idx + R.idx_off;
+  for (int c0 = 0; c0 < n; c0 += kSelThreads) {
+    const int c = c0 + threadIdx.x;
+    const uint32_t key = c < n ? keys[c] : 0u;
+    const int gt = (c < n) && key > prefix;
+    const int eq = (c < n) && key == prefix;
+    int eq_tot;
+    const int eq_rank = eq_base + block_excl_scan(eq, warp_buf, &eq_tot);
+    const int sel = gt || (eq && eq_rank < krem);
+    int sel_tot;
+    const int pos_out = out_base + block_excl_scan(sel, warp_buf, &sel_tot);
+    if (sel) {
+      const int pos = c < bs ? c : c + blk;
+      for (int h = 0; h < H; ++h) out0[(int64_t)h * k + pos_out] = pos;
+    }
+    eq_base += eq_tot;
+    out_base += sel_tot;
+  }
+}
+
 // Debug checker: counts positions out of range, inside the block, or not
 // strictly ascending.
 __global__ void check_indices_kernel(const __grid_constant__ Plan plan, const int32_t *__restrict__ idx,
@@ -186,6 +284,16 @@ cudaError_t launch_select(const Plan &plan, const float *scores, int32_t *idx, c
                                        (int)smem);
   if (e != cudaSuccess) return e;
   select_heads_kernel<<<plan.total_units, kSelThreads, smem, st>>>(plan, scores, idx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select_global(const Plan &plan, const float *scores, int32_t *idx, cudaStream_t st) {
+  int max_n = 0;
+  for (int b = 0; b < plan.nreq; ++b) max_n = max(max_n, plan.r[b].L - (plan.r[b].be - plan.r[b].bs));
+  const size_t smem = (size_t)max(max_n, 1) * sizeof(uint32_t);
+  cudaError_t e = cudaFuncSetAttribute(select_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  select_global_kernel<<<plan.nreq, kSelThreads, smem, st>>>(plan, scores, idx);
   return cudaGetLastError();
 }
 

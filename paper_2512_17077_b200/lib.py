@@ -26,7 +26,7 @@ DLLM_ERR_SHAPE = -3
 DLLM_ERR_K_RANGE = -4
 DLLM_ERR_CUDA = -5
 
-EXPORTED = ("dllm_keep_count", "dllm_index_layout", "dllm_refresh_attn", "dllm_select_heads",
+EXPORTED = ("dllm_keep_count", "dllm_index_layout", "dllm_refresh_attn", "dllm_select_heads", "dllm_select_global",
             "dllm_reuse_sparse_attn", "dllm_check_indices", "dllm_status_string", "dllm_last_error",
             "dllm_version")
 
@@ -71,6 +71,8 @@ def _load() -> ctypes.CDLL:
     lib.dllm_refresh_attn.restype = ctypes.c_int
     lib.dllm_select_heads.argtypes = [P, vp, vp, vp]
     lib.dllm_select_heads.restype = ctypes.c_int
+    lib.dllm_select_global.argtypes = [P, vp, vp, vp]
+    lib.dllm_select_global.restype = ctypes.c_int
     lib.dllm_reuse_sparse_attn.argtypes = [P, vp, vp, vp, vp, vp, vp]
     lib.dllm_reuse_sparse_attn.restype = ctypes.c_int
     lib.dllm_check_indices.argtypes = [P, vp, vp, vp]
@@ -200,6 +202,12 @@ def select_heads(p: Problem, scores, idx, stream=None) -> None:
     """dllm_select_heads (Eq. 6 pool + per-head TopK)."""
     _check(_lib.dllm_select_heads(p.ref, _dev(scores, "scores", torch.float32), _dev(idx, "idx", torch.int32),
                                   _stream(stream)), "dllm_select_heads")
+
+
+def select_global(p: Problem, scores, idx, stream=None) -> None:
+    """dllm_select_global (Eq. 5 uniform baseline: one shared set per request)."""
+    _check(_lib.dllm_select_global(p.ref, _dev(scores, "scores", torch.float32), _dev(idx, "idx", torch.int32),
+                                   _stream(stream)), "dllm_select_global")
 
 
 def reuse_sparse_attn(p: Problem, q_blk, k_cache, v_cache, idx, out_blk, stream=None) -> None:

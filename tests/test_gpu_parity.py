@@ -328,3 +328,58 @@ def test_full_config_hot_path_sampled(L, cfg, sample, r, n):
         assert np.array_equal(idx[b], sel), f"{cfg} selection req {b}"
         ref_u = O.attention_with_cache(f64(batch.q_blk_req(b)), K, V, bs, be, sel)
         assert_close(ob[batch.cu_blk[b]:batch.cu_blk[b + 1]], ref_u, f"{cfg} reuse req {b}")
+
+
+# ------------------------------------------------------------------ N2: uniform (global) selection
+@pytest.mark.parametrize("cfg,n", [("C0", None), ("C1", 4), ("C2", 4), ("C3", 8)])
+def test_select_global_bitexact_integer_scores(L, cfg, n):
+    """dllm_select_global vs the oracle's Eq. 5 selection on integer scores (head sums exact in fp32)."""
+    wl = synth.config(cfg, num_requests=n)
+    p = L.Problem(wl.seq_len, wl.blk_start, wl.blk_end, num_heads=wl.num_heads, num_kv_heads=wl.num_kv_heads,
+                  head_dim=wl.head_dim, keep_ratio=wl.keep_ratio, pool_window=wl.pool_window, page_size=1024,
+                  block_table=torch.zeros((wl.num_requests, 8), dtype=torch.int32).cuda())
+    sc = synth.scores(wl, mode="ties")
+    k, total_idx, _, _ = p.layout()
+    idx = torch.full((max(total_idx, 1),), -7, dtype=torch.int32, device="cuda")
+    L.select_global(p, torch.from_numpy(join_scores(sc)).cuda(), idx)
+    torch.cuda.synchronize()
+    got = split_idx(idx.cpu().numpy()[:total_idx], wl, k)
+    ref = O.select_global_batch([s.astype(np.float64) for s in sc], wl.seq_len, wl.blk_start, wl.blk_end,
+                                wl.keep_ratio, wl.pool_window)
+    for b in range(wl.num_requests):
+        assert all(np.array_equal(got[b][h], ref[b]) for h in range(wl.num_heads)), f"{cfg} req {b}"
+
+
+def test_uniformity_trap_witness_on_gpu(L):
+    """PAPER.md:143-145 / SPEC.md:270: per-head selection keeps every head's top key,
+    the uniform set drops head 1's."""
+    wl = custom("e_trap", [3], [2], [3], H=2, Hk=2, D=16, r=0.5, w=1, P=16)
+    p = L.Problem(wl.seq_len, wl.blk_start, wl.blk_end, num_heads=2, num_kv_heads=2, head_dim=16, keep_ratio=0.5,
+                  pool_window=1, page_size=16, block_table=torch.zeros((1, 1), dtype=torch.int32).cuda())
+    raw = torch.tensor([9.0, 0.0, 5.0, 0.0, 9.0, 5.0], device="cuda")
+    ph = torch.full((2,), -1, dtype=torch.int32, device="cuda")
+    gl = torch.full((2,), -1, dtype=torch.int32, device="cuda")
+    L.select_heads(p, raw, ph)
+    L.select_global(p, raw, gl)
+    torch.cuda.synchronize()
+    assert ph.cpu().tolist() == [0, 1] and gl.cpu().tolist() == [0, 0]
+
+
+def test_uniform_baseline_end_to_end(L):
+    """select_global -> reuse equals the oracle's attention over the shared set (Eq. 4 with one I for all heads)."""
+    batch = synth.make_batch(synth.config("C1", num_requests=2, kind="exact"))
+    wl = batch.wl
+    p, out, scores = _run_refresh(L, batch)
+    k, total_idx, _, _ = p.layout()
+    idx = torch.full((max(total_idx, 1),), -7, dtype=torch.int32, device="cuda")
+    L.select_global(p, torch.from_numpy(np.ascontiguousarray(scores)).cuda(), idx)
+    torch.cuda.synchronize()
+    flat = idx.cpu().numpy()[:total_idx]
+    got_sets = split_idx(flat, wl, k)
+    for b in range(wl.num_requests):
+        qb, K = f64(batch.q_req(b)), f64(batch.k_logical(b))
+        ref = O.select_global(qb[wl.blk_start[b]:wl.blk_end[b]], K, wl.seq_len[b], wl.blk_start[b], wl.blk_end[b],
+                              wl.keep_ratio, wl.pool_window)
+        assert all(np.array_equal(got_sets[b][h], ref) for h in range(wl.num_heads))
+    gotr = _run_reuse(L, batch, p, flat)
+    _check_reuse(batch, gotr, got_sets)

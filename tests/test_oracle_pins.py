@@ -262,3 +262,22 @@ def test_batch_drivers_match_per_request():
     Qb = np.concatenate([Q[3:6], Q[20:21]])
     Ou = O.reuse_batch(Qb, Ks, Vs, bsL, beL, sel)
     assert np.abs(Ou[3:] - O.attention_with_cache(Q[20:21], Ks[1], Vs[1], 8, 9, sel[1])).max() == 0
+
+
+def test_select_global_batch_pins():
+    # H = 1: the uniform sum degenerates to the per-head selection
+    rng = np.random.default_rng(60)
+    sc = [rng.integers(-3, 4, size=(1, 40)).astype(np.float64)]
+    a = O.select_global_batch(sc, [40], [20], [24], 0.3, 3)[0]
+    b = O.select_batch(sc, [40], [20], [24], 0.3, 3)[0][0]
+    assert np.array_equal(a, b)
+    # Uniformity-Trap witness through raw scores: per-head pooled
+    # [[9,0],[0,9]] (w=1), k=1 -> heads keep {0} and {1}; the global sum ties -> {0}
+    raw = [np.array([[9.0, 0.0, 5.0], [0.0, 9.0, 5.0]])]          # position 2 is the block
+    assert O.select_batch(raw, [3], [2], [3], 0.5, 1)[0].tolist() == [[0], [1]]
+    assert O.select_global_batch(raw, [3], [2], [3], 0.5, 1)[0].tolist() == [0]
+    # permuting heads leaves the uniform selection unchanged (a sum), not the per-head one
+    sc = [rng.standard_normal((4, 50))]
+    g1 = O.select_global_batch(sc, [50], [10], [20], 0.4, 3)[0]
+    g2 = O.select_global_batch([sc[0][::-1]], [50], [10], [20], 0.4, 3)[0]
+    assert np.array_equal(g1, g2)
