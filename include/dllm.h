@@ -132,6 +132,21 @@ DLLM_API int dllm_reuse_sparse_attn(const dllm_problem *p, const void *q_blk, co
                            const void *v_cache, const int32_t *idx, void *out_blk,
                            void *stream);
 
+/* Pack (the paper's physical layout, §4.5: "pack the sparse
+ * tokens into a physically dense KV layout", [N_heads, rL, D_head]): for every
+ * (b, h, i), k_pack[(H*cu_k[b] + h*k_b + i) * D + d] = K[idx(b,h,i), kv(h), d]
+ * and likewise V; row order = the idx layout.  k_pack, v_pack: DEVICE bf16
+ * [H * sum_b k_b, D], caller-owned.  idx must satisfy the layout precondition. */
+DLLM_API int dllm_pack_kv(const dllm_problem *p, const void *k_cache, const void *v_cache, const int32_t *idx,
+                          void *k_pack, void *v_pack, void *stream);
+
+/* Reuse over the packed context (Eq. 4 with K_cache = the packed per-head rows,
+ * read contiguously with no index indirection): keys
+ * [bs, be) from the paged cache ++ the k_b packed rows of (b, h).  Same output
+ * as dllm_reuse_sparse_attn on the idx the buffers were packed from. */
+DLLM_API int dllm_reuse_packed(const dllm_problem *p, const void *q_blk, const void *k_cache, const void *v_cache,
+                               const void *k_pack, const void *v_pack, void *out_blk, void *stream);
+
 /* Debug: counts index-layout violations (out of [0, L), inside the block,
  * not strictly ascending) into *d_violations (DEVICE int32, zeroed by the
  * call).  idx, d_violations: DEVICE. */

@@ -24,6 +24,9 @@ namespace dllm {
 cudaError_t launch_select(const Plan &, const float *, int32_t *, cudaStream_t);
 cudaError_t launch_check_indices(const Plan &, const int32_t *, int32_t *, cudaStream_t);
 cudaError_t launch_select_global(const Plan &, const float *, int32_t *, cudaStream_t);
+cudaError_t launch_reuse_packed(const Plan &, const void *, const void *, const void *, const void *, const void *,
+                                void *, cudaStream_t);
+cudaError_t launch_pack_kv(const Plan &, const void *, const void *, const int32_t *, void *, void *, cudaStream_t);
 cudaError_t launch_reuse(const Plan &, const void *, const void *, const void *, const int32_t *, void *,
                          cudaStream_t);
 cudaError_t launch_refresh_mma(const Plan &, const void *, const void *, const void *, void *, float *,
@@ -324,6 +327,53 @@ int dllm_reuse_sparse_attn(const dllm_problem *p, const void *q_blk, const void 
     cudaError_t e = reuse_impl_env() ? launch_reuse_ws(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream)
                                      : launch_reuse(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "reuse launch");
+  }
+  return ok();
+}
+
+int dllm_pack_kv(const dllm_problem *p, const void *k_cache, const void *v_cache, const int32_t *idx, void *k_pack,
+                 void *v_pack, void *stream) {
+  Layout lay;
+  int st = make_layout(p, lay);
+  if (st) return st;
+  const int B = p->num_requests;
+  if (B == 0 || lay.cu_k[B] == 0) return ok();
+  if (!k_cache || !v_cache || !idx || !k_pack || !v_pack) return fail(DLLM_ERR_INVALID_ARG, "pack_kv: NULL pointer");
+  if (!aligned16(k_cache) || !aligned16(v_cache) || !aligned16(k_pack) || !aligned16(v_pack))
+    return fail(DLLM_ERR_SHAPE, "pack_kv: bf16 tensors must be 16-byte aligned");
+  static thread_local Plan pl;
+  for (int b0 = 0; b0 < B; b0 += kMaxReqPerLaunch) {
+    const int b1 = b0 + kMaxReqPerLaunch < B ? b0 + kMaxReqPerLaunch : B;
+    fill_plan(pl, p, lay.k, b0, b1, lay.cu_L, lay.cu_blk, lay.cu_k, [&](int) { return p->num_heads; });
+    cudaError_t e = launch_pack_kv(pl, k_cache, v_cache, idx, k_pack, v_pack, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "pack_kv launch");
+  }
+  return ok();
+}
+
+int dllm_reuse_packed(const dllm_problem *p, const void *q_blk, const void *k_cache, const void *v_cache,
+                      const void *k_pack, const void *v_pack, void *out_blk, void *stream) {
+  Layout lay;
+  int st = make_layout(p, lay);
+  if (st) return st;
+  const int B = p->num_requests;
+  if (B == 0) return ok();
+  if (!q_blk || !k_cache || !v_cache || !out_blk) return fail(DLLM_ERR_INVALID_ARG, "reuse_packed: NULL tensor pointer");
+  if ((!k_pack || !v_pack) && lay.cu_k[B] > 0) return fail(DLLM_ERR_INVALID_ARG, "reuse_packed: NULL packed buffer");
+  if (lay.cu_k[B] * (int64_t)p->num_heads > INT32_MAX)
+    return fail(DLLM_ERR_UNSUPPORTED, "reuse_packed: more than 2^31 packed rows");
+  if (!aligned16(q_blk) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out_blk) ||
+      !aligned16(k_pack) || !aligned16(v_pack))
+    return fail(DLLM_ERR_SHAPE, "reuse_packed: bf16 tensors must be 16-byte aligned");
+  static thread_local Plan pl;
+  for (int b0 = 0; b0 < B; b0 += kMaxReqPerLaunch) {
+    const int b1 = b0 + kMaxReqPerLaunch < B ? b0 + kMaxReqPerLaunch : B;
+    fill_plan(pl, p, lay.k, b0, b1, lay.cu_L, lay.cu_blk, lay.cu_k, [&](int b) {
+      const int blk = p->blk_end[b] - p->blk_start[b];
+      return p->num_heads * ((blk + 31) / 32);
+    });
+    cudaError_t e = launch_reuse_packed(pl, q_blk, k_cache, v_cache, k_pack, v_pack, out_blk, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "reuse_packed launch");
   }
   return ok();
 }

@@ -447,7 +447,6 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
     const uint32_t tO = tmem + lane_off + tmem_o(wg);
     float *sbuf = reinterpret_cast<float *>(gb + C::kOffSc) + wg * (2 * 4 * TBN);
     const float sl2 = plan.scale_log2;
-    const int64_t HD = (int64_t)plan.H * D;
     int sc = 0, oc = 0;
     for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x) {
       Unit u;

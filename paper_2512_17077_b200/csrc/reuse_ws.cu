@@ -87,11 +87,16 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint32_t bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
 }
 
-template <int D>
+// PACKED: the context keys come from the paper's packed per-head buffers
+// (k_pack / v_pack, row = the key's slot in the idx layout, written by
+// dllm_pack_kv) instead of being gathered through the block table; the
+// active block's rows still come from the paged cache.
+template <int D, bool PACKED>
 __global__ void __launch_bounds__(kWsThreads, 1)
 reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restrict__ q_blk,
                 const __nv_bfloat16 *__restrict__ k_cache, const __nv_bfloat16 *__restrict__ v_cache,
-                const int32_t *__restrict__ idx, __nv_bfloat16 *__restrict__ out) {
+                const int32_t *__restrict__ idx, __nv_bfloat16 *__restrict__ out,
+                const __nv_bfloat16 *__restrict__ k_pack, const __nv_bfloat16 *__restrict__ v_pack) {
   using C = WsCfg<D>;
   constexpr int NS = C::kNS;
   constexpr int CH = D / 8;
@@ -159,12 +164,20 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
           const int j = g0 * kChunk + q * 32 + lane;
-          pos[q] = j < u.nk ? (j < u.blk ? u.bs + j : __ldg(my_idx + (j - u.blk))) : -1;
+          if (PACKED)
+            pos[q] = j < u.blk ? u.bs + j : -1;
+          else
+            pos[q] = j < u.nk ? (j < u.blk ? u.bs + j : __ldg(my_idx + (j - u.blk))) : -1;
         }
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
           const int page = pos[q] >= 0 ? __ldg(bt + (pos[q] >> plan.page_shift)) : 0;
           off[q] = pos[q] >= 0 ? (page * plan.H_kv + u.kvh) * plan.page_size + (pos[q] & (plan.page_size - 1)) : -1;
+          if (PACKED) {
+            // packed context rows: slot of the key in the idx layout
+            const int j = g0 * kChunk + q * 32 + lane;
+            if (j >= u.blk && j < u.nk) off[q] = (int)(u.idx_off + (j - u.blk));
+          }
         }
         const int ng = min(kTG, nchunks - g0);
 #pragma unroll
@@ -204,8 +217,9 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
           const int off = offs[slot * kChunk + r];
           const int64_t goff = (int64_t)(off < 0 ? 0 : off) * D + cc * 8;
           const int nb = off < 0 ? 0 : 16;
-          cp_async16(smem_u32(dk + r * C::kRowB + cc * 16), k_cache + goff, nb);
-          cp_async16(smem_u32(dv + r * C::kRowB + cc * 16), v_cache + goff, nb);
+          const bool from_pack = PACKED && (c * kChunk + r) >= u.blk;
+          cp_async16(smem_u32(dk + r * C::kRowB + cc * 16), (from_pack ? k_pack : k_cache) + goff, nb);
+          cp_async16(smem_u32(dv + r * C::kRowB + cc * 16), (from_pack ? v_pack : v_cache) + goff, nb);
         }
         cp_async_mbar_arrive_noinc(b_full + 8 * s);
         __syncwarp();
@@ -377,17 +391,55 @@ int num_sms_ws() {
   return n;
 }
 
-template <int D>
+template <int D, bool PACKED>
 cudaError_t launch_ws_d(const Plan &plan, const void *q_blk, const void *k_cache, const void *v_cache,
-                        const int32_t *idx, void *out, cudaStream_t st) {
+                        const int32_t *idx, void *out, const void *k_pack, const void *v_pack, cudaStream_t st) {
   const int smem = WsCfg<D>::kBytes;
-  cudaError_t e = cudaFuncSetAttribute(reuse_ws_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(reuse_ws_kernel<D, PACKED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int grid = plan.total_units < num_sms_ws() ? plan.total_units : num_sms_ws();
   if (grid <= 0) return cudaSuccess;
-  reuse_ws_kernel<D><<<grid, kWsThreads, smem, st>>>(plan, (const __nv_bfloat16 *)q_blk,
-                                                     (const __nv_bfloat16 *)k_cache, (const __nv_bfloat16 *)v_cache,
-                                                     idx, (__nv_bfloat16 *)out);
+  reuse_ws_kernel<D, PACKED><<<grid, kWsThreads, smem, st>>>(
+      plan, (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k_cache, (const __nv_bfloat16 *)v_cache, idx,
+      (__nv_bfloat16 *)out, (const __nv_bfloat16 *)k_pack, (const __nv_bfloat16 *)v_pack);
+  return cudaGetLastError();
+}
+
+// Pack (§4.5): the selected K/V rows of every (b, h) copied
+// into dense per-head buffers, row order = the idx layout.  One CTA per (b, h);
+// 16-byte loads through the block table, 16-byte stores.
+template <int D>
+__global__ void __launch_bounds__(256)
+pack_kv_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restrict__ k_cache,
+               const __nv_bfloat16 *__restrict__ v_cache, const int32_t *__restrict__ idx,
+               __nv_bfloat16 *__restrict__ k_pack, __nv_bfloat16 *__restrict__ v_pack) {
+  constexpr int CH = D / 8;
+  const int unit = blockIdx.x;
+  const int b = plan_find(plan, unit);
+  const ReqInfo &R = plan.r[b];
+  const int h = unit - R.unit_off;
+  const int kvh = h / (plan.H / plan.H_kv);
+  const int64_t row0 = R.idx_off + (int64_t)h * R.k;
+  const int32_t *bt = plan.block_table + (int64_t)R.bt_row * plan.pages_per_req;
+#pragma unroll 4
+  for (int e = threadIdx.x; e < R.k * CH; e += blockDim.x) {
+    const int i = e / CH, cc = e - i * CH;
+    const int pos = __ldg(idx + row0 + i);
+    const int page = __ldg(bt + (pos >> plan.page_shift));
+    const int64_t src = (((int64_t)page * plan.H_kv + kvh) * plan.page_size + (pos & (plan.page_size - 1))) * D + cc * 8;
+    const int64_t dst = (row0 + i) * D + cc * 8;
+    *reinterpret_cast<uint4 *>(k_pack + dst) = __ldg(reinterpret_cast<const uint4 *>(k_cache + src));
+    *reinterpret_cast<uint4 *>(v_pack + dst) = __ldg(reinterpret_cast<const uint4 *>(v_cache + src));
+  }
+}
+
+template <int D>
+cudaError_t launch_pack_d(const Plan &plan, const void *k_cache, const void *v_cache, const int32_t *idx,
+                          void *k_pack, void *v_pack, cudaStream_t st) {
+  if (plan.total_units <= 0) return cudaSuccess;
+  pack_kv_kernel<D><<<plan.total_units, 256, 0, st>>>(plan, (const __nv_bfloat16 *)k_cache,
+                                                      (const __nv_bfloat16 *)v_cache, idx, (__nv_bfloat16 *)k_pack,
+                                                      (__nv_bfloat16 *)v_pack);
   return cudaGetLastError();
 }
 
@@ -396,10 +448,32 @@ cudaError_t launch_ws_d(const Plan &plan, const void *q_blk, const void *k_cache
 cudaError_t launch_reuse_ws(const Plan &plan, const void *q_blk, const void *k_cache, const void *v_cache,
                             const int32_t *idx, void *out, cudaStream_t st) {
   switch (plan.D) {
-    case 16: return launch_ws_d<16>(plan, q_blk, k_cache, v_cache, idx, out, st);
-    case 32: return launch_ws_d<32>(plan, q_blk, k_cache, v_cache, idx, out, st);
-    case 64: return launch_ws_d<64>(plan, q_blk, k_cache, v_cache, idx, out, st);
-    case 128: return launch_ws_d<128>(plan, q_blk, k_cache, v_cache, idx, out, st);
+    case 16: return launch_ws_d<16, false>(plan, q_blk, k_cache, v_cache, idx, out, nullptr, nullptr, st);
+    case 32: return launch_ws_d<32, false>(plan, q_blk, k_cache, v_cache, idx, out, nullptr, nullptr, st);
+    case 64: return launch_ws_d<64, false>(plan, q_blk, k_cache, v_cache, idx, out, nullptr, nullptr, st);
+    case 128: return launch_ws_d<128, false>(plan, q_blk, k_cache, v_cache, idx, out, nullptr, nullptr, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_reuse_packed(const Plan &plan, const void *q_blk, const void *k_cache, const void *v_cache,
+                                const void *k_pack, const void *v_pack, void *out, cudaStream_t st) {
+  switch (plan.D) {
+    case 16: return launch_ws_d<16, true>(plan, q_blk, k_cache, v_cache, nullptr, out, k_pack, v_pack, st);
+    case 32: return launch_ws_d<32, true>(plan, q_blk, k_cache, v_cache, nullptr, out, k_pack, v_pack, st);
+    case 64: return launch_ws_d<64, true>(plan, q_blk, k_cache, v_cache, nullptr, out, k_pack, v_pack, st);
+    case 128: return launch_ws_d<128, true>(plan, q_blk, k_cache, v_cache, nullptr, out, k_pack, v_pack, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_pack_kv(const Plan &plan, const void *k_cache, const void *v_cache, const int32_t *idx,
+                           void *k_pack, void *v_pack, cudaStream_t st) {
+  switch (plan.D) {
+    case 16: return launch_pack_d<16>(plan, k_cache, v_cache, idx, k_pack, v_pack, st);
+    case 32: return launch_pack_d<32>(plan, k_cache, v_cache, idx, k_pack, v_pack, st);
+    case 64: return launch_pack_d<64>(plan, k_cache, v_cache, idx, k_pack, v_pack, st);
+    case 128: return launch_pack_d<128>(plan, k_cache, v_cache, idx, k_pack, v_pack, st);
   }
   return cudaErrorInvalidValue;
 }

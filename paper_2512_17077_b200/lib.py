@@ -27,7 +27,7 @@ DLLM_ERR_K_RANGE = -4
 DLLM_ERR_CUDA = -5
 
 EXPORTED = ("dllm_keep_count", "dllm_index_layout", "dllm_refresh_attn", "dllm_select_heads", "dllm_select_global",
-            "dllm_reuse_sparse_attn", "dllm_check_indices", "dllm_status_string", "dllm_last_error",
+            "dllm_reuse_sparse_attn", "dllm_pack_kv", "dllm_reuse_packed", "dllm_check_indices", "dllm_status_string", "dllm_last_error",
             "dllm_version")
 
 
@@ -75,6 +75,10 @@ def _load() -> ctypes.CDLL:
     lib.dllm_select_global.restype = ctypes.c_int
     lib.dllm_reuse_sparse_attn.argtypes = [P, vp, vp, vp, vp, vp, vp]
     lib.dllm_reuse_sparse_attn.restype = ctypes.c_int
+    lib.dllm_pack_kv.argtypes = [P, vp, vp, vp, vp, vp, vp]
+    lib.dllm_pack_kv.restype = ctypes.c_int
+    lib.dllm_reuse_packed.argtypes = [P, vp, vp, vp, vp, vp, vp, vp]
+    lib.dllm_reuse_packed.restype = ctypes.c_int
     lib.dllm_check_indices.argtypes = [P, vp, vp, vp]
     lib.dllm_check_indices.restype = ctypes.c_int
     lib.dllm_status_string.argtypes = [ctypes.c_int]
@@ -216,6 +220,22 @@ def reuse_sparse_attn(p: Problem, q_blk, k_cache, v_cache, idx, out_blk, stream=
     _check(_lib.dllm_reuse_sparse_attn(p.ref, _dev(q_blk, "q_blk", bf), _dev(k_cache, "k_cache", bf),
                                        _dev(v_cache, "v_cache", bf), _dev(idx, "idx", torch.int32),
                                        _dev(out_blk, "out_blk", bf), _stream(stream)), "dllm_reuse_sparse_attn")
+
+
+def pack_kv(p: Problem, k_cache, v_cache, idx, k_pack, v_pack, stream=None) -> None:
+    """dllm_pack_kv (the paper's dense per-head layout)."""
+    bf = torch.bfloat16
+    _check(_lib.dllm_pack_kv(p.ref, _dev(k_cache, "k_cache", bf), _dev(v_cache, "v_cache", bf),
+                             _dev(idx, "idx", torch.int32), _dev(k_pack, "k_pack", bf), _dev(v_pack, "v_pack", bf),
+                             _stream(stream)), "dllm_pack_kv")
+
+
+def reuse_packed(p: Problem, q_blk, k_cache, v_cache, k_pack, v_pack, out_blk, stream=None) -> None:
+    """dllm_reuse_packed (Eq. 4 over the packed per-head context)."""
+    bf = torch.bfloat16
+    _check(_lib.dllm_reuse_packed(p.ref, _dev(q_blk, "q_blk", bf), _dev(k_cache, "k_cache", bf),
+                                  _dev(v_cache, "v_cache", bf), _dev(k_pack, "k_pack", bf), _dev(v_pack, "v_pack", bf),
+                                  _dev(out_blk, "out_blk", bf), _stream(stream)), "dllm_reuse_packed")
 
 
 def check_indices(p: Problem, idx, violations, stream=None) -> None:

@@ -50,6 +50,11 @@ def main():
         "select": lambda: lib.select_heads(p, buf.scores, buf.idx),
         "reuse": lambda: lib.reuse_sparse_attn(p, qb, kc, vc, buf.idx, buf.out_blk),
     }
+    k_, total_idx_, _, _ = p.layout()
+    kp = torch.empty((max(total_idx_, 1), wl.head_dim), dtype=torch.bfloat16, device="cuda")
+    vp = torch.empty_like(kp)
+    fns["pack"] = lambda: lib.pack_kv(p, kc, vc, buf.idx, kp, vp)
+    fns["reuse_packed"] = lambda: lib.reuse_packed(p, qb, kc, vc, kp, vp, buf.out_blk)
     for f in fns.values():
         f()
     torch.cuda.synchronize()
@@ -76,6 +81,11 @@ def main():
     t = res["reuse"][0]
     print(f"{args.cfg} reuse  : {t*1e6:.1f} us  {ub/t/1e9:.1f} GB/s unique ({lb/t/1e9:.1f} logical), "
           f"unique {ub/1e6:.1f} MB")
+    t = res["pack"][0]
+    pb = 2 * 2 * total_idx * wl.head_dim * 2
+    print(f"{args.cfg} pack   : {t*1e6:.1f} us  {pb/t/1e9:.1f} GB/s (read+write {pb/1e6:.1f} MB)")
+    t = res["reuse_packed"][0]
+    print(f"{args.cfg} reuse_packed: {t*1e6:.1f} us  {lb/t/1e9:.1f} GB/s logical")
     print(lib.version())
 
 

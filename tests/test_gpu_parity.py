@@ -383,3 +383,38 @@ def test_uniform_baseline_end_to_end(L):
         assert all(np.array_equal(got_sets[b][h], ref) for h in range(wl.num_heads))
     gotr = _run_reuse(L, batch, p, flat)
     _check_reuse(batch, gotr, got_sets)
+
+
+# ------------------------------------------------------------------ N1: pack-at-Refresh layout
+@pytest.mark.parametrize("cfg,n", [("C0", None), ("C1", 3), ("C2", 3)])
+def test_pack_and_reuse_packed(L, cfg, n):
+    """dllm_pack_kv copies exactly the selected rows (bit-identical gathering) and
+    dllm_reuse_packed equals the gather-in-place Reuse bit for bit (same keys, same order)."""
+    batch = synth.make_batch(synth.config(cfg, num_requests=n))
+    wl = batch.wl
+    p = problem_of(batch)
+    k = oracle_keep_counts(wl)
+    idx_list = synth.indices(wl, k)
+    flat = join_idx(idx_list)
+    q, q_blk, kc, vc = to_dev(batch)
+    _, total_idx, _, blk_rows = p.layout()
+    idx = torch.from_numpy(flat).cuda()
+    kp = torch.full((total_idx, wl.head_dim), float("nan"), dtype=torch.bfloat16, device="cuda")
+    vp = torch.full_like(kp, float("nan"))
+    L.pack_kv(p, kc, vc, idx, kp, vp)
+    out_p = torch.full((blk_rows, wl.num_heads, wl.head_dim), float("nan"), dtype=torch.bfloat16, device="cuda")
+    L.reuse_packed(p, q_blk, kc, vc, kp, vp, out_p)
+    torch.cuda.synchronize()
+    kp_h, vp_h = kp.cpu(), vp.cpu()
+    off = 0
+    g = wl.num_heads // wl.num_kv_heads
+    for b in range(wl.num_requests):
+        Kl, Vl = batch.k_logical(b), batch.v_logical(b)
+        for h in range(wl.num_heads):
+            rows = torch.from_numpy(idx_list[b][h].astype(np.int64))
+            assert torch.equal(kp_h[off:off + k[b]].view(torch.int16), Kl[rows, h // g].view(torch.int16))
+            assert torch.equal(vp_h[off:off + k[b]].view(torch.int16), Vl[rows, h // g].view(torch.int16))
+            off += k[b]
+    out_g = _run_reuse(L, batch, p, flat)
+    assert np.array_equal(out_p.float().cpu().numpy().view(np.uint32), out_g.view(np.uint32))
+    _check_reuse(batch, out_p.float().cpu().numpy(), idx_list)
