@@ -132,7 +132,7 @@ __device__ __forceinline__ void decode_unit(const Plan &pl, const ReqInfo *rs, i
   const int npairs = (ntiles + 1) >> 1;
   const int local = unit - R.unit_off;
   u.h = local / npairs;
-  const int p = local - u.h * npairs;
+  const int p = (local - u.h * npairs + u.h) % npairs;   // rotate pairs by head (see refresh_tc2.cu)
   u.kvh = u.h / (pl.H / pl.H_kv);
   u.n = (u.L + TBN - 1) / TBN;
 #pragma unroll
@@ -286,7 +286,7 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
   } else if (warp == 1) {
     // ============================ MMA issuer ============================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 104;\n" ::: "memory");
-    if (lane == 0) {
+    {
       constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(TBM, TBN, false, false);
       constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(TBM, D, false, true);
       int it = 0, ucnt = 0, vzc = 0, pc[2] = {0, 0};
@@ -300,7 +300,7 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
             const uint32_t off = (uint32_t)((k >> 2) * TBM * 128 + (k & 3) * 32);
             const uint64_t a = ptx::smem_desc_sw128(sb + C::kOffQ + i * C::kQBytes + off, 16, 1024);
             const uint64_t b = ptx::smem_desc_sw128(sb + C::kOffK + stage * C::kKVBytes + off, 16, 1024);
-            ptx::mma_ss(tmem + tmem_s(i), a, b, idesc_qk, k > 0);
+            ptx::mma_ss_elect(tmem + tmem_s(i), a, b, idesc_qk, k > 0);
           }
         };
         auto pv = [&](int i, int stage, bool acc) {
@@ -308,7 +308,7 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
           for (int k = 0; k < TBN / 16; ++k) {
             const uint64_t b = ptx::smem_desc_sw128(sb + C::kOffV + stage * C::kKVBytes + k * 16 * 128,
                                                     TBN * 128, 1024);
-            ptx::mma_ts(tmem + tmem_o(i), tmem + tmem_s(i) + (uint32_t)(k * 8), b, idesc_pv, (acc || k > 0) ? 1u : 0u);
+            ptx::mma_ts_elect(tmem + tmem_o(i), tmem + tmem_s(i) + (uint32_t)(k * 8), b, idesc_pv, (acc || k > 0) ? 1u : 0u);
           }
         };
         ptx::mbar_wait(bar(B_QFULL), ucnt & 1);
@@ -318,56 +318,56 @@ refresh_tc_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUt
           ptx::mbar_wait(bar(B_KFULL + s0), (it >> 1) & 1);
           ptx::tc_fence_after();
           qk(0, s0);
-          ptx::mma_commit(bar(B_SFULL + 0));
+          ptx::mma_commit_elect(bar(B_SFULL + 0));
           if (two) {
             qk(1, s0);
-            ptx::mma_commit(bar(B_SFULL + 1));
+            ptx::mma_commit_elect(bar(B_SFULL + 1));
           }
-          ptx::mma_commit(bar(B_KEMPTY + s0));
-          if (u.n == 1) ptx::mma_commit(bar(B_QEMPTY));
+          ptx::mma_commit_elect(bar(B_KEMPTY + s0));
+          if (u.n == 1) ptx::mma_commit_elect(bar(B_QEMPTY));
         }
         for (int j = 0; j < u.n; ++j) {
           const int s = (it + j) & 1;
           const bool has_next = j + 1 < u.n;
           const int sn = (it + j + 1) & 1;
-          TRACE(10, it + j);
+          if (lane == 0) TRACE(10, it + j);
           ptx::mbar_wait(bar(B_VFULL + s), ((it + j) >> 1) & 1);
           if (j == u.n - 1 && (u.L % TBN) != 0) {
             ptx::mbar_wait(bar(B_VZ), vzc & 1);
             ++vzc;
           }
-          TRACE(11, it + j);
+          if (lane == 0) TRACE(11, it + j);
           ptx::tc_fence_after();
-          TRACE(6, pc[0]);
+          if (lane == 0) TRACE(6, pc[0]);
           ptx::mbar_wait(bar(B_PFULL + 0), pc[0] & 1);
-          TRACE(7, pc[0]);
+          if (lane == 0) TRACE(7, pc[0]);
           ++pc[0];
           ptx::tc_fence_after();
           pv(0, s, j > 0);
-          if (!has_next) ptx::mma_commit(bar(B_OFULL + 0));
+          if (!has_next) ptx::mma_commit_elect(bar(B_OFULL + 0));
           if (has_next) {
             ptx::mbar_wait(bar(B_KFULL + sn), ((it + j + 1) >> 1) & 1);
             ptx::tc_fence_after();
             qk(0, sn);
-            ptx::mma_commit(bar(B_SFULL + 0));
-            if (!two && j + 1 == u.n - 1) ptx::mma_commit(bar(B_QEMPTY));
+            ptx::mma_commit_elect(bar(B_SFULL + 0));
+            if (!two && j + 1 == u.n - 1) ptx::mma_commit_elect(bar(B_QEMPTY));
           }
           if (two) {
-            TRACE(8, pc[1]);
+            if (lane == 0) TRACE(8, pc[1]);
             ptx::mbar_wait(bar(B_PFULL + 1), pc[1] & 1);
-            TRACE(9, pc[1]);
+            if (lane == 0) TRACE(9, pc[1]);
             ++pc[1];
             ptx::tc_fence_after();
             pv(1, s, j > 0);
-            if (!has_next) ptx::mma_commit(bar(B_OFULL + 1));
+            if (!has_next) ptx::mma_commit_elect(bar(B_OFULL + 1));
             if (has_next) {
               qk(1, sn);
-              ptx::mma_commit(bar(B_SFULL + 1));
-              if (j + 1 == u.n - 1) ptx::mma_commit(bar(B_QEMPTY));
+              ptx::mma_commit_elect(bar(B_SFULL + 1));
+              if (j + 1 == u.n - 1) ptx::mma_commit_elect(bar(B_QEMPTY));
             }
           }
-          if (has_next) ptx::mma_commit(bar(B_KEMPTY + sn));
-          ptx::mma_commit(bar(B_VEMPTY + s));
+          if (has_next) ptx::mma_commit_elect(bar(B_KEMPTY + sn));
+          ptx::mma_commit_elect(bar(B_VEMPTY + s));
         }
         it += u.n;
       }

@@ -76,6 +76,12 @@ constexpr int kPrefetchSteps = DLLM_TC2_PREFETCH;   // next-unit K/V steps warme
 #define DLLM_TC2_NEXTDECODE 0
 #endif
 constexpr bool kNextDecode = DLLM_TC2_NEXTDECODE;  // decode the next unit mid-unit (producer / MMA / Q warps)
+#ifndef DLLM_TC2_KVMERGED
+#define DLLM_TC2_KVMERGED 0
+#endif
+// one barrier pair per K/V stage (K and V of a step land together, the stage is
+// released after the step's P.V): one wait and one commit fewer per step
+constexpr bool kKVMerged = DLLM_TC2_KVMERGED;
 
 template <int D>
 struct Cfg {
@@ -266,7 +272,7 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
           for (int sbx = 0; sbx < nsub; ++sbx) nvalid += (sbx * boxrows < key_end);
           const uint32_t bytes = (uint32_t)(nvalid * C::kChunks) * boxbytes;
           ptx::mbar_wait(bar(B_KEMPTY + s), ph ^ 1);
-          ptx::mbar_arrive_expect_tx(bar(B_KFULL + s), bytes);
+          ptx::mbar_arrive_expect_tx(bar(B_KFULL + s), kKVMerged ? 2 * bytes : bytes);
           for (int sbx = 0; sbx < nvalid; ++sbx) {
             const int key0 = j * TBN + sbx * boxrows;
             const int page = __ldg(bt + (key0 >> plan.page_shift));
@@ -275,22 +281,24 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
               ptx::tma_load_4d(sb + C::kOffK + s * C::kKVBytes + c * TBN * 128 + sbx * boxrows * 128, &tm_k,
                                bar(B_KFULL + s), c * 64, slot, u.kvh, page);
           }
-          ptx::mbar_wait(bar(B_VEMPTY + s), ph ^ 1);
-          ptx::mbar_arrive_expect_tx(bar(B_VFULL + s), bytes);
+          if (!kKVMerged) {
+            ptx::mbar_wait(bar(B_VEMPTY + s), ph ^ 1);
+            ptx::mbar_arrive_expect_tx(bar(B_VFULL + s), bytes);
+          }
           for (int sbx = 0; sbx < nvalid; ++sbx) {
             const int key0 = j * TBN + sbx * boxrows;
             const int page = __ldg(bt + (key0 >> plan.page_shift));
             const int slot = key0 & (plan.page_size - 1);
             for (int c = 0; c < C::kChunks; ++c)
               ptx::tma_load_4d(sb + C::kOffV + s * C::kKVBytes + c * TBN * 128 + sbx * boxrows * 128, &tm_v,
-                               bar(B_VFULL + s), c * 64, slot, u.kvh, page);
+                               bar((kKVMerged ? B_KFULL : B_VFULL) + s), c * 64, slot, u.kvh, page);
           }
         }
         __syncwarp();
         if (kNextDecode && j == 0 && unit + (int)gridDim.x < plan.total_units) decode_unit(plan, rs, unit + gridDim.x, un);
         if (key_end < TBN) {
           // zero V rows >= key_end (P is 0 there, but 0 * NaN would poison O)
-          ptx::mbar_wait(bar(B_VFULL + s), ph);
+          ptx::mbar_wait(bar((kKVMerged ? B_KFULL : B_VFULL) + s), ph);
           uint8_t *vbase = gb + C::kOffV + s * C::kKVBytes;
           const int nrow = TBN - key_end;
           for (int e = lane; e < nrow * 8 * C::kChunks; e += 32) {
@@ -389,14 +397,14 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
           if (lane == 0) TRACE2(18 + jj, ucnt);
           ptx::tc_fence_after();
           for (int i = 0; i < nt; ++i) qk(i, st);
-          ptx::mma_commit_elect(bar(B_KEMPTY + st));
+          if (!kKVMerged) ptx::mma_commit_elect(bar(B_KEMPTY + st));
         }
         if (u.n <= 2) ptx::mma_commit_elect(bar(B_QEMPTY));
         if (kNextDecode && unit + (int)gridDim.x < plan.total_units) decode_unit(plan, rs, unit + gridDim.x, un);
         for (int j = 0; j < u.n; ++j) {
           const int sv = (it + j) % NST;
           if (lane == 0) TRACE2(10, it + j);
-          ptx::mbar_wait(bar(B_VFULL + sv), ((it + j) / NST) & 1);
+          if (!kKVMerged) ptx::mbar_wait(bar(B_VFULL + sv), ((it + j) / NST) & 1);
           if (lane == 0) TRACE2(11, it + j);
           if (j == u.n - 1 && (u.L % TBN) != 0) {
             ptx::mbar_wait(bar(B_VZ), vzc & 1);
@@ -427,10 +435,10 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
             }
           }
           if (ahead) {
-            ptx::mma_commit_elect(bar(B_KEMPTY + sk));
+            if (!kKVMerged) ptx::mma_commit_elect(bar(B_KEMPTY + sk));
             if (j + 2 == u.n - 1) ptx::mma_commit_elect(bar(B_QEMPTY));
           }
-          ptx::mma_commit_elect(bar(B_VEMPTY + sv));
+          ptx::mma_commit_elect(bar((kKVMerged ? B_KEMPTY : B_VEMPTY) + sv));
           if (lane == 0 && j == u.n - 1) TRACE2(22, ucnt);
         }
         it += u.n;
