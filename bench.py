@@ -56,7 +56,9 @@ def load_peaks():
 
 
 def workload_desc(wl, n):
-    return (f"{wl.name}: {wl.num_requests} requests/GPU x {n} GPU, H={wl.num_heads}, H_kv={wl.num_kv_heads}, "
+    mix = "" if wl.refresh_mask is None else \
+        f" ({sum(wl.refresh_mask)} Refresh+select+Reuse, {wl.num_requests - sum(wl.refresh_mask)} Reuse-only)"
+    return (f"{wl.name}: {wl.num_requests} requests/GPU{mix} x {n} GPU, H={wl.num_heads}, H_kv={wl.num_kv_heads}, "
             f"D={wl.head_dim}, L={min(wl.seq_len)}..{max(wl.seq_len)}, blk={wl.blk[0]}, r={wl.keep_ratio}, "
             f"w={wl.pool_window}, page={wl.page_size}")
 
@@ -107,30 +109,51 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- oracle (CPU) timing
 def cpu_oracle_rate(wl, budget_s: float = 12.0, max_requests: int | None = None):
     """The fp64 oracle as it stands, on a bounded sample of the workload's
-    requests (whole requests: Refresh + importance + select + Reuse, all heads).
-    Returns (requests/s, requests timed, seconds, threads)."""
+    requests (whole requests: Refresh + importance + select + Reuse, all heads;
+    in a mixed batch the reuse-only requests run Reuse alone on the same index
+    lists the GPU arm uses).  Returns (requests/s, requests timed, seconds, threads).
+    For a mixed batch the rate is the batch's request count over the batch time
+    extrapolated from the per-kind mean request times of the sample."""
     import torch
 
     import oracle as O
     from paper_2512_17077_b200 import synth
     cores = len(os.sched_getaffinity(0))
     torch.set_num_threads(cores)
+    mask = wl.refresh_mask or [True] * wl.num_requests
+    kinds = sorted(set(mask), reverse=True)
+    order = [[b for b in range(wl.num_requests) if mask[b] == kd] for kd in kinds]
+    per_kind = {}
     done, t_total = 0, 0.0
-    b = 0
-    while b < wl.num_requests and (max_requests is None or done < max_requests):
-        q, K, V, qb = (t.double().numpy() for t in synth.request_tensors(wl, b))
-        bs, be, L = wl.blk_start[b], wl.blk_end[b], wl.seq_len[b]
-        t0 = time.perf_counter()
-        O.attention_dense(q, K, V)
-        raw = O.raw_scores(q[bs:be], K)
-        sel = O.select_batch([raw], [L], [bs], [be], wl.keep_ratio, wl.pool_window)[0]
-        O.attention_with_cache(qb, K, V, bs, be, sel)
-        t_total += time.perf_counter() - t0
-        done += 1
-        b += 1
-        if t_total >= budget_s:
-            break
-    return done / t_total, done, t_total, cores
+    for kd, reqs in zip(kinds, order):
+        t_kind, n_kind = 0.0, 0
+        for b in reqs:
+            if max_requests is not None and done >= max_requests:
+                break
+            q, K, V, qb = (t.double().numpy() for t in synth.request_tensors(wl, b))
+            bs, be, L = wl.blk_start[b], wl.blk_end[b], wl.seq_len[b]
+            if not kd:
+                k = O.keep_count(wl.keep_ratio, L - (be - bs))
+                sel = synth.indices(synth.subset(wl, [b]), [k])[0]
+            t0 = time.perf_counter()
+            if kd:
+                O.attention_dense(q, K, V)
+                raw = O.raw_scores(q[bs:be], K)
+                sel = O.select_batch([raw], [L], [bs], [be], wl.keep_ratio, wl.pool_window)[0]
+            O.attention_with_cache(qb, K, V, bs, be, sel)
+            dt = time.perf_counter() - t0
+            t_kind += dt
+            t_total += dt
+            n_kind += 1
+            done += 1
+            if t_kind >= budget_s / len(kinds):
+                break
+        if n_kind:
+            per_kind[kd] = t_kind / n_kind
+    if len(kinds) == 1:
+        return done / t_total, done, t_total, cores
+    t_batch = sum(per_kind.get(kd, 0.0) * len(reqs) for kd, reqs in zip(kinds, order))
+    return wl.num_requests / t_batch, done, t_total, cores
 
 
 # ----------------------------------------------------------------------------- ncu traffic
@@ -211,28 +234,52 @@ def main():
              for L, s, e, k in zip(glob.seq_len, glob.blk_start, glob.blk_end, k_glob)]
     parts = shard.lpt_partition(costs, world)
     wl = synth.subset(glob, parts[rank])
-    batch = synth.make_batch(wl)
-
-    p = lib.Problem(wl.seq_len, wl.blk_start, wl.blk_end, num_heads=wl.num_heads, num_kv_heads=wl.num_kv_heads,
-                    head_dim=wl.head_dim, keep_ratio=wl.keep_ratio, pool_window=wl.pool_window,
-                    page_size=wl.page_size, block_table=batch.block_table.to(dev))
-    q, qb, kc, vc = (t.to(dev) for t in (batch.q, batch.q_blk, batch.k_cache, batch.v_cache))
-    buf = lib.alloc_buffers(p, device=dev)
-    k, total_idx, rows, blk_rows = p.layout()
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    n_launch_per_call = (wl.num_requests + 255) // 256
+
+    # A step runs Refresh -> select -> Reuse for every request, except in a mixed
+    # (burst) batch (C3: refresh_mask), where only the Refresh requests run
+    # Refresh + select + Reuse and the others run Reuse alone with the index
+    # lists of an earlier selection (generated once, outside the timed region).
+    def make_part(sub, refresh):
+        bt = synth.make_batch(sub)
+        pp = lib.Problem(sub.seq_len, sub.blk_start, sub.blk_end, num_heads=sub.num_heads,
+                         num_kv_heads=sub.num_kv_heads, head_dim=sub.head_dim, keep_ratio=sub.keep_ratio,
+                         pool_window=sub.pool_window, page_size=sub.page_size, block_table=bt.block_table.to(dev))
+        tens = [t.to(dev) for t in (bt.q, bt.q_blk, bt.k_cache, bt.v_cache)]
+        bf = lib.alloc_buffers(pp, device=dev)
+        if not refresh:
+            kk = pp.layout()[0]
+            flat = np.concatenate([x.reshape(-1) for x in synth.indices(sub, kk)]).astype(np.int32)
+            if flat.size:
+                bf.idx[:flat.size].copy_(torch.from_numpy(flat))
+        return {"wl": sub, "batch": bt, "p": pp, "t": tens, "buf": bf, "refresh": refresh}
+
+    if wl.refresh_mask is None:
+        parts_local = [make_part(wl, True)]
+    else:
+        ri = [i for i, m in enumerate(wl.refresh_mask) if m]
+        ui = [i for i, m in enumerate(wl.refresh_mask) if not m]
+        parts_local = ([make_part(synth.subset(wl, ri), True)] if ri else []) + \
+                      ([make_part(synth.subset(wl, ui), False)] if ui else [])
 
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
-        lib.refresh_attn(p, q, kc, vc, buf.out, buf.scores, stream)
+        for pt in parts_local:
+            if pt["refresh"]:
+                q, qb, kc, vc = pt["t"]
+                lib.refresh_attn(pt["p"], q, kc, vc, pt["buf"].out, pt["buf"].scores, stream)
         if ev is not None:
             ev[1].record(stream)
-        lib.select_heads(p, buf.scores, buf.idx, stream)
+        for pt in parts_local:
+            if pt["refresh"]:
+                lib.select_heads(pt["p"], pt["buf"].scores, pt["buf"].idx, stream)
         if ev is not None:
             ev[2].record(stream)
-        lib.reuse_sparse_attn(p, qb, kc, vc, buf.idx, buf.out_blk, stream)
+        for pt in parts_local:
+            q, qb, kc, vc = pt["t"]
+            lib.reuse_sparse_attn(pt["p"], qb, kc, vc, pt["buf"].idx, pt["buf"].out_blk, stream)
         if ev is not None:
             ev[3].record(stream)
 
@@ -265,26 +312,41 @@ def main():
 
     # ---- algorithmic work per launch
     H, Hk, D = wl.num_heads, wl.num_kv_heads, wl.head_dim
-    flops_refresh = sum(4.0 * H * L * L * D for L in wl.seq_len)
-    idx_host = buf.idx[:total_idx].cpu().numpy()
     g = H // Hk
-    uniq_rows, off = 0, 0
-    for b in range(wl.num_requests):
-        rows_b = idx_host[off:off + H * k[b]].reshape(H, k[b])
-        off += H * k[b]
-        for kv in range(Hk):
-            uniq_rows += len(np.unique(rows_b[kv * g:(kv + 1) * g])) + wl.blk[b]
-    reuse_bytes = uniq_rows * 2 * D * 2 + 2 * blk_rows * H * D * 2 + 4 * total_idx
-    reuse_logical = sum(H * (wl.blk[b] + k[b]) for b in range(wl.num_requests)) * 2 * D * 2 + \
-        2 * blk_rows * H * D * 2 + 4 * total_idx
-    select_bytes = 4 * H * rows + 4 * total_idx
-    a_ref = flops_refresh / statistics.mean(t_ref) / 1e12
+    flops_refresh = 0.0
+    reuse_bytes = reuse_logical = select_bytes = 0
+    total_idx_all = rows_all = 0
+    for pt in parts_local:
+        sub = pt["wl"]
+        kk, total_idx, rows, blk_rows = pt["p"].layout()
+        idx_host = pt["buf"].idx[:total_idx].cpu().numpy()
+        uniq_rows, off = 0, 0
+        for b in range(sub.num_requests):
+            rows_b = idx_host[off:off + H * kk[b]].reshape(H, kk[b])
+            off += H * kk[b]
+            for kv in range(Hk):
+                uniq_rows += len(np.unique(rows_b[kv * g:(kv + 1) * g])) + sub.blk[b]
+        reuse_bytes += uniq_rows * 2 * D * 2 + 2 * blk_rows * H * D * 2 + 4 * total_idx
+        reuse_logical += sum(H * (sub.blk[b] + kk[b]) for b in range(sub.num_requests)) * 2 * D * 2 + \
+            2 * blk_rows * H * D * 2 + 4 * total_idx
+        if pt["refresh"]:
+            flops_refresh += sum(4.0 * H * L * L * D for L in sub.seq_len)
+            select_bytes += 4 * H * rows + 4 * total_idx
+        total_idx_all += total_idx
+        rows_all += rows
+    a_ref = flops_refresh / statistics.mean(t_ref) / 1e12 if flops_refresh else 0.0
     a_reu = reuse_bytes / statistics.mean(t_reu) / 1e9
-    a_sel = select_bytes / statistics.mean(t_sel) / 1e9
+    a_sel = select_bytes / statistics.mean(t_sel) / 1e9 if select_bytes else 0.0
+    main_part = parts_local[0]
+    buf = main_part["buf"]
+    batch = main_part["batch"]
+    q, qb, kc, vc = main_part["t"]
+    p = main_part["p"]
+    k, total_idx, rows, blk_rows = p.layout()
 
     # ---- all-gather of per-request outputs (NCCL), timed separately
     allgather_ms = None
-    if world > 1:
+    if world > 1 and len(parts_local) == 1:
         counts_rows = [sum(glob.seq_len[i] for i in parts[r]) for r in range(world)]
         counts_blk = [sum(glob.blk[i] for i in parts[r]) for r in range(world)]
         for _ in range(2):
@@ -304,11 +366,21 @@ def main():
 
     # ---- end to end through the public API with host buffers
     pin = lambda t: t.pin_memory()  # noqa: E731
-    h_in = [pin(batch.q), pin(batch.q_blk), pin(batch.k_cache), pin(batch.v_cache)]
-    h_out = [torch.empty(buf.out.shape, dtype=buf.out.dtype).pin_memory(),
-             torch.empty(buf.out_blk.shape, dtype=buf.out_blk.dtype).pin_memory(),
-             torch.empty((max(total_idx, 1),), dtype=torch.int32).pin_memory()]
-    d_in = [q, qb, kc, vc]
+    h_in, d_in, h_out, d_out = [], [], [], []
+    for pt in parts_local:
+        bt, tb, (_, tidx, _, _) = pt["batch"], pt["buf"], pt["p"].layout()
+        h_in += [pin(bt.q_blk), pin(bt.k_cache), pin(bt.v_cache)]
+        d_in += pt["t"][1:]
+        if pt["refresh"]:
+            h_in.append(pin(bt.q))
+            d_in.append(pt["t"][0])
+            d_out += [tb.out, tb.idx[:max(tidx, 1)]]
+        else:
+            # reuse-only requests bring the index lists of their earlier selection
+            h_in.append(tb.idx[:max(tidx, 1)].cpu().pin_memory())
+            d_in.append(tb.idx[:max(tidx, 1)])
+        d_out.append(tb.out_blk)
+    h_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in d_out]
     h2d = sum(t.numel() * t.element_size() for t in h_in)
     d2h = sum(t.numel() * t.element_size() for t in h_out)
 
@@ -316,9 +388,8 @@ def main():
         for d, h in zip(d_in, h_in):
             d.copy_(h, non_blocking=True)
         step()
-        h_out[0].copy_(buf.out, non_blocking=True)
-        h_out[1].copy_(buf.out_blk, non_blocking=True)
-        h_out[2].copy_(buf.idx[:max(total_idx, 1)], non_blocking=True)
+        for h, d in zip(h_out, d_out):
+            h.copy_(d, non_blocking=True)
 
     e2e_step()
     torch.cuda.synchronize(dev)
@@ -367,10 +438,12 @@ def main():
                           "bytes_per_launch_unique": reuse_bytes, "bytes_per_launch_logical": reuse_logical,
                           "GB/s_logical": reuse_logical / statistics.mean(t_reu) / 1e9, "bound": "hbm",
                           "peak": hbm_peak},
-                "block_cycle_us": 1e6 * (statistics.mean(t_ref) + statistics.mean(t_sel) + 31 * statistics.mean(t_reu)),
+                "block_cycle_us": (1e6 * (statistics.mean(t_ref) + statistics.mean(t_sel) + 31 * statistics.mean(t_reu))
+                                   if len(parts_local) == 1 and parts_local[0]["refresh"] else None),
             },
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": 3 * n_launch_per_call * args.steps,
+            "gpu_launches": sum((3 if pt["refresh"] else 1) * ((pt["wl"].num_requests + 255) // 256)
+                                for pt in parts_local) * args.steps,
             "clocks": clocks,
             "cpu_baseline": cpu,
             "allgather_ms": allgather_ms,

@@ -276,7 +276,8 @@ def indices(wl: Workload, k_per_request: Sequence[int], seed: Optional[int] = No
     for b, k in enumerate(k_per_request):
         L, bs, be = wl.seq_len[b], wl.blk_start[b], wl.blk_end[b]
         pool = np.concatenate([np.arange(0, bs), np.arange(be, L)])
-        rng = np.random.default_rng(_subseed(seed, wl.name, "idx", b, mode))
+        rid = b if wl.req_ids is None else wl.req_ids[b]
+        rng = np.random.default_rng(_subseed(seed, wl.name, "idx", rid, mode))
         rows = []
         g = wl.num_heads // wl.num_kv_heads
         for h in range(wl.num_heads):
