@@ -33,6 +33,9 @@ cudaError_t launch_refresh_mma(const Plan &, const void *, const void *, const v
                                cudaStream_t);
 cudaError_t launch_reuse_ws(const Plan &, const void *, const void *, const void *, const int32_t *, void *,
                             cudaStream_t);
+bool reuse_tc_supported(int D);
+cudaError_t launch_reuse_tc(const Plan &, const void *, const void *, const void *, const int32_t *, void *,
+                            cudaStream_t);
 int refresh_mma_units(int L, int bs, int be, int H, bool with_scores);
 bool refresh_tc_supported(int D);
 int refresh_tc2_units(int L, int bs, int be, int H, bool with_scores);
@@ -193,10 +196,13 @@ int cuda_fail(cudaError_t e, const char *what) {
 }
 
 int reuse_impl_env() {
-  // DLLM_REUSE_IMPL=v1 selects the one-CTA-per-unit kernel (A/B comparisons).
+  // DLLM_REUSE_IMPL=v1 | ws selects the one-CTA-per-unit mma.sync kernel or the
+  // persistent mma.sync kernel (A/B comparisons); default: tcgen05 (D = 128),
+  // else the persistent mma.sync kernel.
   const char *s = getenv("DLLM_REUSE_IMPL");
   if (s && !strcmp(s, "v1")) return 0;
-  return 1;
+  if (s && !strcmp(s, "ws")) return 1;
+  return 2;
 }
 
 int refresh_impl_env() {
@@ -324,8 +330,12 @@ int dllm_reuse_sparse_attn(const dllm_problem *p, const void *q_blk, const void 
       const int blk = p->blk_end[b] - p->blk_start[b];
       return p->num_heads * ((blk + 31) / 32);
     });
-    cudaError_t e = reuse_impl_env() ? launch_reuse_ws(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream)
-                                     : launch_reuse(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream);
+    const int impl = reuse_impl_env();
+    cudaError_t e =
+        impl == 2 && reuse_tc_supported(p->head_dim)
+            ? launch_reuse_tc(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream)
+        : impl >= 1 ? launch_reuse_ws(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream)
+                    : launch_reuse(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "reuse launch");
   }
   return ok();

@@ -10,7 +10,10 @@
 
 namespace dllm {
 
-constexpr int kMaxReqPerLaunch = 256;
+#ifndef DLLM_MAX_REQ
+#define DLLM_MAX_REQ 256
+#endif
+constexpr int kMaxReqPerLaunch = DLLM_MAX_REQ;
 
 struct ReqInfo {
   int32_t L;         // sequence length L_b

@@ -38,6 +38,12 @@ constexpr int kWsConsumers = 4;
 #ifndef DLLM_RWS_NS
 #define DLLM_RWS_NS 4
 #endif
+#ifndef DLLM_RWS_L2PF
+#define DLLM_RWS_L2PF 1  // L2 prefetch of the CTA's index lists / block-table rows at start
+#endif
+#ifndef DLLM_RWS_DBG
+#define DLLM_RWS_DBG 0   // dev only: 1 = consumers skip the math, 2 = loaders skip the gathers
+#endif
 constexpr int kLoaders = DLLM_RWS_LOADERS;   // cp.async issuing warps
 constexpr int kWsThreads = (kWsConsumers + 1 + kLoaders) * 32;
 constexpr int kRows = 32;          // query rows per unit
@@ -60,6 +66,42 @@ struct WsCfg {
   static constexpr int kOffBar = kOffX + 2 * 32 * kXStride * 4;
   static constexpr int kBytes = kOffBar + 8 * (2 * kNS + 2 * kNT + 4) + 128;
 };
+
+#ifdef DLLM_TRACE
+// per-CTA timeline (globaltimer ns): [0] start, [1] translator: first offsets
+// published, [2] consumer: first chunk ready, [3..10] consumer: end of unit i,
+// [11] end, [12] SM id
+__device__ long long g_rws[1024][16];
+extern "C" __attribute__((visibility("default"))) int dllm_trace_rws_read(long long *host) {
+  return (int)cudaMemcpyFromSymbol(host, g_rws, sizeof(g_rws));
+}
+__device__ __forceinline__ long long rws_timer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// CTA 0 per-chunk timeline: [0] translator published, [1] loader issued,
+// [2] consumer: data ready, [3] consumer: chunk done, [4] consumer: wait start
+__device__ long long g_rws_chunk[5][64];
+extern "C" __attribute__((visibility("default"))) int dllm_trace_rws_chunk(long long *host) {
+  return (int)cudaMemcpyFromSymbol(host, g_rws_chunk, sizeof(g_rws_chunk));
+}
+#define RWS_CHUNK(kind, t)                                                               \
+  do {                                                                                   \
+    if (lane == 0 && blockIdx.x == 0 && (t) < 64) g_rws_chunk[kind][t] = rws_timer();    \
+  } while (0)
+#define RWS_TRACE(slot)                                                                  \
+  do {                                                                                   \
+    if (lane == 0 && blockIdx.x < 1024) g_rws[blockIdx.x][slot] = rws_timer();           \
+  } while (0)
+#else
+#define RWS_TRACE(slot) \
+  do {                  \
+  } while (0)
+#define RWS_CHUNK(kind, t) \
+  do {                     \
+  } while (0)
+#endif
 
 struct RUnit {
   int b, h, kvh, rg, blk, bs, nk, k, blk_off, bt_row;
@@ -113,6 +155,15 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
   const uint32_t b_qempty = b_qfull + 16;                     // [2] consumers (4)
   int32_t *offs = reinterpret_cast<int32_t *>(smem + C::kOffOffs);
 
+#ifdef DLLM_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 1024) {
+    for (int i = 0; i < 16; ++i) g_rws[blockIdx.x][i] = 0;
+    g_rws[blockIdx.x][0] = rws_timer();
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_rws[blockIdx.x][12] = smid;
+  }
+#endif
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
       ptx::mbar_init(b_full + 8 * i, 32 * kLoaders);
@@ -132,6 +183,25 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
 
   if (warp == kWsConsumers) {
     // ============================ translator (+ Q rows) ============================
+#if DLLM_RWS_L2PF
+    // every index list and block-table row this CTA will translate, pulled into
+    // L2 up front: the per-unit translation is two dependent memory round trips
+    // (idx, then block table), and with few units per CTA they are the critical path
+    for (int unit = blockIdx.x + lane * gridDim.x; unit < plan.total_units; unit += 32 * gridDim.x) {
+      RUnit u;
+      decode(plan, unit, u);
+      if (!PACKED && u.k > 0) {
+        const uintptr_t a0 = reinterpret_cast<uintptr_t>(idx + u.idx_off) & ~uintptr_t(15);
+        const uintptr_t a1 = (reinterpret_cast<uintptr_t>(idx + u.idx_off + u.k) + 15) & ~uintptr_t(15);
+        ptx::bulk_prefetch_l2(reinterpret_cast<const void *>(a0), (uint32_t)(a1 - a0));
+      }
+      const uintptr_t b0 = reinterpret_cast<uintptr_t>(plan.block_table + (int64_t)u.bt_row * plan.pages_per_req) &
+                           ~uintptr_t(15);
+      const uintptr_t b1 = (reinterpret_cast<uintptr_t>(plan.block_table + (int64_t)(u.bt_row + 1) * plan.pages_per_req) +
+                            15) & ~uintptr_t(15);
+      ptx::bulk_prefetch_l2(reinterpret_cast<const void *>(b0), (uint32_t)(b1 - b0));
+    }
+#endif
     int t = 0, qc = 0;
     for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x) {
       RUnit u;
@@ -189,6 +259,8 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
           for (int rr = 0; rr < kChunk / 32; ++rr) offs[slot * kChunk + rr * 32 + lane] = off[c * (kChunk / 32) + rr];
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(b_ofull + 8 * slot);
+          if (t == 0) RWS_TRACE(1);
+          RWS_CHUNK(0, t);
           ++t;
         }
       }
@@ -212,7 +284,7 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
         // of the same 2D-byte row (coalesced per row); rows past the key list are
         // zero-filled (src-size 0); completion counted with cp.async.mbarrier.arrive.noinc
 #pragma unroll 4
-        for (int e = li * 32 + lane; e < kChunk * CH; e += 32 * kLoaders) {
+        for (int e = li * 32 + lane; e < (DLLM_RWS_DBG == 2 ? 0 : kChunk * CH); e += 32 * kLoaders) {
           const int r = e / CH, cc = e - r * CH;
           const int off = offs[slot * kChunk + r];
           const int64_t goff = (int64_t)(off < 0 ? 0 : off) * D + cc * 8;
@@ -224,6 +296,7 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
         cp_async_mbar_arrive_noinc(b_full + 8 * s);
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(b_oempty + 8 * slot);
+        if (li == 0) RWS_CHUNK(1, t);
       }
     }
     cp_async_wait<0>();
@@ -258,7 +331,15 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
 
       for (int c = 0; c < nchunks; ++c, ++t) {
         const int s = t % NS;
+        if (warp == 0) RWS_CHUNK(4, t);
         ptx::mbar_wait(b_full + 8 * s, (t / NS) & 1);
+        if (t == 0 && warp == 0) RWS_TRACE(2);
+        if (warp == 0) RWS_CHUNK(2, t);
+        if (DLLM_RWS_DBG == 1) {
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(b_empty + 8 * s);
+          continue;
+        }
         const uint8_t *tk = smem + C::kOffK + s * C::kKV;
         const uint8_t *tv = smem + C::kOffV + s * C::kKV;
         float sc[4][4];
@@ -333,6 +414,7 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
         }
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(b_empty + 8 * s);
+        if (warp == 0) RWS_CHUNK(3, t);
       }
       // ---- merge the two key halves and store
 #pragma unroll
@@ -376,7 +458,9 @@ reuse_ws_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
         }
       }
       ptx::named_bar_sync(1, kWsConsumers * 32);      // merge buffer free for the next unit
+      if (warp == 0 && qc < 8) RWS_TRACE(3 + qc);
     }
+    if (warp == 0) RWS_TRACE(11);
   }
 }
 

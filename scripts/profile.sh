@@ -9,7 +9,7 @@ mkdir -p $OUT
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
     --log-file $OUT/launches_$CFG.csv \
     python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $OUT/bench_under_ncu.log 2>&1
-for k in refresh_tc2 reuse_ws select_heads; do
+for k in ${KERNELS:-refresh_tc2 reuse_tc select_heads}; do
   ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 -o $OUT/prof_${CFG}_$k -f \
       python scripts/kbench.py $CFG --iters 2 > $OUT/ncu_$k.log 2>&1
 done
