@@ -207,6 +207,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph replay")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -264,6 +265,7 @@ def main():
                       ([make_part(synth.subset(wl, ui), False)] if ui else [])
 
     def step(ev=None):
+        stream = torch.cuda.current_stream(dev)   # the capture stream while a graph is recorded
         if ev is not None:
             ev[0].record(stream)
         for pt in parts_local:
@@ -302,7 +304,40 @@ def main():
     t_sel = [evs[i][1].elapsed_time(evs[i][2]) * 1e-3 for i in range(args.steps)]
     t_reu = [evs[i][2].elapsed_time(evs[i][3]) * 1e-3 for i in range(args.steps)]
     t_step = [evs[i][0].elapsed_time(evs[i][3]) * 1e-3 for i in range(args.steps)]
-    total = sum(t_step)
+    total_eager = sum(t_step)
+    total = total_eager
+    launch_mode = "eager"
+    if not args.no_graph:
+        # the step's launches captured once in a CUDA graph (requests/s
+        # without launch gaps); each replay is one full step on the same buffers
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream(dev)
+        cs.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(cs):
+            step()   # warm the capture stream
+        torch.cuda.current_stream(dev).wait_stream(cs)
+        torch.cuda.synchronize(dev)
+        with torch.cuda.graph(g, stream=cs):
+            step()
+        for _ in range(args.warmup):
+            flush.zero_()
+            g.replay()
+        torch.cuda.synchronize(dev)
+        gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        with ClockSampler(local_rank) as clk:
+            for i in range(args.steps):
+                flush.zero_()
+                gev[i][0].record(stream)
+                g.replay()
+                gev[i][1].record(stream)
+            torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        total = sum(gev[i][0].elapsed_time(gev[i][1]) * 1e-3 for i in range(args.steps))
+        launch_mode = "cuda_graph"
     tt = torch.tensor([total], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -441,6 +476,8 @@ def main():
                 "block_cycle_us": (1e6 * (statistics.mean(t_ref) + statistics.mean(t_sel) + 31 * statistics.mean(t_reu))
                                    if len(parts_local) == 1 and parts_local[0]["refresh"] else None),
             },
+            "launch_mode": launch_mode,
+            "ms_per_step_eager": 1e3 * total_eager / args.steps,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": sum((3 if pt["refresh"] else 1) * ((pt["wl"].num_requests + 255) // 256)
                                 for pt in parts_local) * args.steps,

@@ -82,7 +82,9 @@ constexpr int kOffOffs = kOffQ + 2 * kQTile;    // [kTNT][kTChunk] int32
 constexpr int kOffRed = kOffOffs + kTNT * kTChunk * 4;   // [4 warps][32] chunk row maxima
 constexpr int kOffL = kOffRed + 4 * 32 * 4;            // [2 O buffers][4 warps][32 rows] partial row sums
 constexpr int kOffStage = kOffL + 2 * 4 * 32 * 4;      // output staging [32 rows][D] bf16
-constexpr int kOffBar = kOffStage + kTRows * kTD * 2;
+constexpr int kBtMax = 1024;                          // block-table entries cached in shared memory
+constexpr int kOffBt = kOffStage + kTRows * kTD * 2;  // [kBtMax] int32
+constexpr int kOffBar = kOffBt + kBtMax * 4;
 constexpr int kNumBars = 2 * kTNS + 2 * kTNT + 2 + 2 + 2 + 2 + 2 + 1 + 2 + 2 + 2 + 1;
 constexpr int kTBytes = kOffBar + 8 * kNumBars + 1024;   // + alignment slack
 static_assert(kTBytes <= 227 * 1024, "reuse_tc shared memory");
@@ -276,13 +278,15 @@ reuse_tc_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
           ~uintptr_t(15);
       ptx::bulk_prefetch_l2(reinterpret_cast<const void *>(b0), (uint32_t)(b1 - b0));
     }
-    int t = 0;
+    int t = 0, bt_cached = -1;
+    int *bts = reinterpret_cast<int *>(gb + kOffBt);
     for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x) {
       TUnit u;
       tdecode(plan, unit, u);
       const int32_t *my_idx = idx + u.idx_off;
       const int32_t *bt = plan.block_table + (int64_t)u.bt_row * plan.pages_per_req;
       const int nchunks = (u.nk + kTChunk - 1) / kTChunk;
+      const bool bt_smem = plan.pages_per_req <= kBtMax;
       for (int g0 = 0; g0 < nchunks; g0 += kTTG) {
         constexpr int Q = kTTG * kTChunk / 32;
         int pos[Q], off[Q];
@@ -291,9 +295,30 @@ reuse_tc_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restri
           const int j = g0 * kTChunk + q * 32 + lane;
           pos[q] = j < u.nk ? (j < u.blk ? u.bs + j : __ldg(my_idx + (j - u.blk))) : -1;
         }
+        if (g0 == 0 && bt_smem && u.bt_row != bt_cached) {
+          // the request's block-table row goes to shared memory while the index loads
+          // above are in flight: a translation costs one memory round trip, not two
+          __syncwarp();
+          for (int i0 = 0; i0 < plan.pages_per_req; i0 += 8 * 32) {
+            int v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int i = i0 + q * 32 + lane;
+              v[q] = i < plan.pages_per_req ? __ldg(bt + i) : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int i = i0 + q * 32 + lane;
+              if (i < plan.pages_per_req) bts[i] = v[q];
+            }
+          }
+          bt_cached = u.bt_row;
+        }
+        __syncwarp();
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-          const int page = pos[q] >= 0 ? __ldg(bt + (pos[q] >> plan.page_shift)) : 0;
+          const int pi = pos[q] >= 0 ? (pos[q] >> plan.page_shift) : 0;
+          const int page = pos[q] >= 0 ? (bt_smem ? bts[pi] : __ldg(bt + pi)) : 0;
           off[q] = pos[q] >= 0 ? (page * plan.H_kv + u.kvh) * plan.page_size + (pos[q] & (plan.page_size - 1)) : -1;
         }
         const int ng = min(kTTG, nchunks - g0);
