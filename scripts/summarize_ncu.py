@@ -12,7 +12,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 src, cfg, rnd = sys.argv[1], sys.argv[2], sys.argv[3]
-KERNELS = {"refresh": "refresh_tc2", "reuse": "reuse_ws", "select": "select_heads"}
+KERNELS = {"refresh": "refresh_tc2", "reuse": "reuse_tc", "select": "select_heads"}
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
