@@ -147,6 +147,40 @@ DLLM_API int dllm_pack_kv(const dllm_problem *p, const void *k_cache, const void
 DLLM_API int dllm_reuse_packed(const dllm_problem *p, const void *q_blk, const void *k_cache, const void *v_cache,
                                const void *k_pack, const void *v_pack, void *out_blk, void *stream);
 
+/* ---- Logit decomposition (next row N4; §4.3 "Logit
+ * Decomposition", §5; SPEC.md:145-165 plan_logit_chunks /
+ * chunked_decode).  The LM head in token chunks of at most max_num_logits rows,
+ * each chunk decoded by ArgMax before the next. ---- */
+
+/* plan_logit_chunks: greedy full chunks of max_num_logits
+ * followed by one remainder chunk, covering [0, n_logit) in order.  Writes up to
+ * `capacity` sizes into chunk_sizes (HOST, may be NULL when capacity is 0) and
+ * returns the number of chunks (>= 0), or DLLM_ERR_INVALID_ARG if n_logit < 0,
+ * max_num_logits < 1 or the chunks do not fit in `capacity`. */
+DLLM_API int dllm_logit_chunks(int64_t n_logit, int32_t max_num_logits, int32_t *chunk_sizes, int32_t capacity);
+
+/* Bytes of DEVICE workspace dllm_lm_head_argmax needs: one 8-byte (max, index)
+ * partial per (row of a chunk, 256-wide vocabulary tile), i.e.
+ * min(n_tok, max_num_logits) * ceil(vocab / 256) * 8.  Negative on bad args. */
+DLLM_API int64_t dllm_lm_head_workspace_bytes(int32_t n_tok, int32_t vocab, int32_t max_num_logits);
+
+/* chunked_decode with ArgMax: for every token row i,
+ *   ids[i] = argmax_v sum_k hidden[i,k] * weight[v,k]     (fp32 accumulation
+ *   of the bf16 products; ties -> the LOWEST v),
+ * processing the rows in the chunks of dllm_logit_chunks(n_tok,
+ * max_num_logits).  The [chunk, vocab] logits are never written to memory:
+ * every 128 x 256 logit tile is reduced in the tensor-core accumulator and only
+ * per-tile (max, index) partials reach the workspace.
+ *   hidden:  DEVICE bf16 [n_tok, d_model] row-major (token-major), 16-B aligned
+ *   weight:  DEVICE bf16 [vocab, d_model] row-major (nn.Linear layout)
+ *   ids:     DEVICE int32 [n_tok], written
+ *   workspace: DEVICE, >= dllm_lm_head_workspace_bytes(...) bytes, caller-owned
+ * d_model must be a positive multiple of 64; vocab >= 1; n_tok >= 0 (0 is a
+ * no-op).  Returns DLLM_OK or a negative status; nothing is enqueued on error. */
+DLLM_API int dllm_lm_head_argmax(const void *hidden, const void *weight, int32_t n_tok, int32_t d_model,
+                                 int32_t vocab, int32_t max_num_logits, int32_t *ids, void *workspace,
+                                 int64_t workspace_bytes, void *stream);
+
 /* Debug: counts index-layout violations (out of [0, L), inside the block,
  * not strictly ascending) into *d_violations (DEVICE int32, zeroed by the
  * call).  idx, d_violations: DEVICE. */

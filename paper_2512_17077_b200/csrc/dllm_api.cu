@@ -33,6 +33,9 @@ cudaError_t launch_refresh_mma(const Plan &, const void *, const void *, const v
                                cudaStream_t);
 cudaError_t launch_reuse_ws(const Plan &, const void *, const void *, const void *, const int32_t *, void *,
                             cudaStream_t);
+int64_t lmhead_vocab_tiles(int vocab);
+cudaError_t launch_lmhead_chunk(const void *hidden, const void *weight, int n_tok, int d_model, int vocab, int row0,
+                                int n_rows, int32_t *ids, void *workspace, cudaStream_t st);
 bool reuse_tc_supported(int D);
 cudaError_t launch_reuse_tc(const Plan &, const void *, const void *, const void *, const int32_t *, void *,
                             cudaStream_t);
@@ -404,6 +407,55 @@ int dllm_check_indices(const dllm_problem *p, const int32_t *idx, int32_t *d_vio
     fill_plan(pl, p, lay.k, b0, b1, lay.cu_L, lay.cu_blk, lay.cu_k, [&](int) { return p->num_heads; });
     e = launch_check_indices(pl, idx, d_violations, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "check_indices launch");
+  }
+  return ok();
+}
+
+int dllm_logit_chunks(int64_t n_logit, int32_t max_num_logits, int32_t *chunk_sizes, int32_t capacity) {
+  if (n_logit < 0 || max_num_logits < 1 || capacity < 0)
+    return fail(DLLM_ERR_INVALID_ARG, "logit_chunks: n_logit %lld, max_num_logits %d, capacity %d",
+                (long long)n_logit, max_num_logits, capacity);
+  const int64_t n = (n_logit + max_num_logits - 1) / max_num_logits;
+  if (n > capacity && (capacity > 0 || chunk_sizes))
+    return fail(DLLM_ERR_INVALID_ARG, "logit_chunks: %lld chunks do not fit capacity %d", (long long)n, capacity);
+  if (n > 0x7fffffff) return fail(DLLM_ERR_INVALID_ARG, "logit_chunks: too many chunks");
+  for (int64_t i = 0; chunk_sizes && i < n; ++i) {
+    const int64_t left = n_logit - i * max_num_logits;
+    chunk_sizes[i] = (int32_t)(left < max_num_logits ? left : max_num_logits);
+  }
+  ok();
+  return (int)n;
+}
+
+int64_t dllm_lm_head_workspace_bytes(int32_t n_tok, int32_t vocab, int32_t max_num_logits) {
+  if (n_tok < 0 || vocab < 1 || max_num_logits < 1)
+    return fail(DLLM_ERR_INVALID_ARG, "lm_head_workspace_bytes: n_tok %d, vocab %d, max_num_logits %d", n_tok, vocab,
+                max_num_logits);
+  const int64_t rows = n_tok < max_num_logits ? n_tok : max_num_logits;
+  return rows * lmhead_vocab_tiles(vocab) * 8;
+}
+
+int dllm_lm_head_argmax(const void *hidden, const void *weight, int32_t n_tok, int32_t d_model, int32_t vocab,
+                        int32_t max_num_logits, int32_t *ids, void *workspace, int64_t workspace_bytes,
+                        void *stream) {
+  if (n_tok < 0 || vocab < 1 || max_num_logits < 1 || d_model < 64 || d_model % 64)
+    return fail(d_model > 0 && d_model % 64 ? DLLM_ERR_UNSUPPORTED : DLLM_ERR_INVALID_ARG,
+                "lm_head_argmax: n_tok %d, d_model %d (multiple of 64), vocab %d, max_num_logits %d", n_tok, d_model,
+                vocab, max_num_logits);
+  if (n_tok == 0) return ok();
+  if (!hidden || !weight || !ids || !workspace)
+    return fail(DLLM_ERR_INVALID_ARG, "lm_head_argmax: NULL buffer");
+  if (((uintptr_t)hidden | (uintptr_t)weight | (uintptr_t)workspace) & 15)
+    return fail(DLLM_ERR_SHAPE, "lm_head_argmax: hidden / weight / workspace not 16-byte aligned");
+  const int64_t need = dllm_lm_head_workspace_bytes(n_tok, vocab, max_num_logits);
+  if (workspace_bytes < need)
+    return fail(DLLM_ERR_INVALID_ARG, "lm_head_argmax: workspace %lld bytes < %lld", (long long)workspace_bytes,
+                (long long)need);
+  for (int64_t r0 = 0; r0 < n_tok; r0 += max_num_logits) {
+    const int rows = (int)(n_tok - r0 < max_num_logits ? n_tok - r0 : max_num_logits);
+    cudaError_t e = launch_lmhead_chunk(hidden, weight, n_tok, d_model, vocab, (int)r0, rows, ids, workspace,
+                                        (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "lm_head_argmax launch");
   }
   return ok();
 }

@@ -27,8 +27,9 @@ DLLM_ERR_K_RANGE = -4
 DLLM_ERR_CUDA = -5
 
 EXPORTED = ("dllm_keep_count", "dllm_index_layout", "dllm_refresh_attn", "dllm_select_heads", "dllm_select_global",
-            "dllm_reuse_sparse_attn", "dllm_pack_kv", "dllm_reuse_packed", "dllm_check_indices", "dllm_status_string", "dllm_last_error",
-            "dllm_version")
+            "dllm_reuse_sparse_attn", "dllm_pack_kv", "dllm_reuse_packed", "dllm_logit_chunks",
+            "dllm_lm_head_workspace_bytes", "dllm_lm_head_argmax", "dllm_check_indices", "dllm_status_string",
+            "dllm_last_error", "dllm_version")
 
 
 class DllmError(RuntimeError):
@@ -79,6 +80,13 @@ def _load() -> ctypes.CDLL:
     lib.dllm_pack_kv.restype = ctypes.c_int
     lib.dllm_reuse_packed.argtypes = [P, vp, vp, vp, vp, vp, vp, vp]
     lib.dllm_reuse_packed.restype = ctypes.c_int
+    lib.dllm_logit_chunks.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.c_int32]
+    lib.dllm_logit_chunks.restype = ctypes.c_int
+    lib.dllm_lm_head_workspace_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
+    lib.dllm_lm_head_workspace_bytes.restype = ctypes.c_int64
+    lib.dllm_lm_head_argmax.argtypes = [vp, vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp, vp,
+                                        ctypes.c_int64, vp]
+    lib.dllm_lm_head_argmax.restype = ctypes.c_int
     lib.dllm_check_indices.argtypes = [P, vp, vp, vp]
     lib.dllm_check_indices.restype = ctypes.c_int
     lib.dllm_status_string.argtypes = [ctypes.c_int]
@@ -236,6 +244,38 @@ def reuse_packed(p: Problem, q_blk, k_cache, v_cache, k_pack, v_pack, out_blk, s
     _check(_lib.dllm_reuse_packed(p.ref, _dev(q_blk, "q_blk", bf), _dev(k_cache, "k_cache", bf),
                                   _dev(v_cache, "v_cache", bf), _dev(k_pack, "k_pack", bf), _dev(v_pack, "v_pack", bf),
                                   _dev(out_blk, "out_blk", bf), _stream(stream)), "dllm_reuse_packed")
+
+
+def logit_chunks(n_logit: int, max_num_logits: int) -> list:
+    """SPEC.md:145-155 plan_logit_chunks through the C-ABI (host only)."""
+    n = _lib.dllm_logit_chunks(int(n_logit), int(max_num_logits), None, 0)
+    _check(min(n, 0), "dllm_logit_chunks")
+    buf = (ctypes.c_int32 * max(n, 1))()
+    n2 = _lib.dllm_logit_chunks(int(n_logit), int(max_num_logits), buf, n)
+    _check(min(n2, 0), "dllm_logit_chunks")
+    return [int(buf[i]) for i in range(n2)]
+
+
+def lm_head_workspace_bytes(n_tok: int, vocab: int, max_num_logits: int) -> int:
+    b = _lib.dllm_lm_head_workspace_bytes(int(n_tok), int(vocab), int(max_num_logits))
+    _check(int(min(b, 0)), "dllm_lm_head_workspace_bytes")
+    return int(b)
+
+
+def lm_head_argmax(hidden, weight, ids, max_num_logits: int = 2048, workspace=None, stream=None) -> None:
+    """ids[i] = lowest-index argmax_v hidden[i] . weight[v] (N4)."""
+    n_tok, d_model = hidden.shape
+    vocab = weight.shape[0]
+    if weight.shape[1] != d_model:
+        raise ValueError("weight must be [vocab, d_model]")
+    if workspace is None:
+        workspace = torch.empty(max(lm_head_workspace_bytes(n_tok, vocab, max_num_logits), 16), dtype=torch.uint8,
+                                device=hidden.device)
+    bf = torch.bfloat16
+    _check(_lib.dllm_lm_head_argmax(_dev(hidden, "hidden", bf), _dev(weight, "weight", bf), int(n_tok), int(d_model),
+                                    int(vocab), int(max_num_logits), _dev(ids, "ids", torch.int32),
+                                    _dev(workspace, "workspace"), int(workspace.numel() * workspace.element_size()),
+                                    _stream(stream)), "dllm_lm_head_argmax")
 
 
 def check_indices(p: Problem, idx, violations, stream=None) -> None:

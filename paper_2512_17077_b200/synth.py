@@ -34,7 +34,7 @@ import numpy as np
 import torch
 
 __all__ = ["Workload", "config", "CONFIG_NAMES", "request_tensors", "Batch", "make_batch",
-           "indices", "scores", "replicate", "subset"]
+           "indices", "scores", "replicate", "subset", "lm_head_inputs", "LM_HEAD_FULL"]
 
 
 def _subseed(*parts) -> int:
@@ -310,3 +310,30 @@ def scores(wl: Workload, seed: Optional[int] = None, mode: str = "ties") -> List
             raise KeyError(mode)
         out.append(s)
     return out
+
+
+# ----------------------------------------------------------------------------- N4 inputs
+# LM-head shapes (Table 3: at most 2,048 materialised logit rows;
+# LLaDA-8B: d_model 4,096, vocabulary 126,464 -- the published model config).
+LM_HEAD_FULL = {"n_tok": 2048, "d_model": 4096, "vocab": 126464, "max_num_logits": 2048}
+
+
+def lm_head_inputs(n_tok: int, d_model: int, vocab: int, kind: str = "realistic", seed: Optional[int] = None):
+    """(hidden [n_tok, d_model], weight [vocab, d_model]) bf16 CPU tensors.
+
+    realistic: hidden ~ N(0, 1) (post-norm hidden states), weight ~ N(0, 0.02^2)
+    (LM-head scale).  exact: integers in [-2, 2] for both, so every logit is an
+    integer of magnitude <= 4 d_model, exact in fp32 under any summation order,
+    with many exact ties (the lowest-index rule is exercised)."""
+    seed = base_seed() if seed is None else seed
+    gh = _gen(_subseed(seed, "lm_head", n_tok, d_model, vocab, kind, "hidden"))
+    gw = _gen(_subseed(seed, "lm_head", n_tok, d_model, vocab, kind, "weight"))
+    if kind == "exact":
+        h = torch.randint(-2, 3, (n_tok, d_model), generator=gh).float()
+        w = torch.randint(-2, 3, (vocab, d_model), generator=gw).float()
+    elif kind == "realistic":
+        h = torch.randn((n_tok, d_model), generator=gh)
+        w = torch.randn((vocab, d_model), generator=gw) * 0.02
+    else:
+        raise ValueError(kind)
+    return _bf16(h), _bf16(w)

@@ -138,3 +138,32 @@ def test_binding_refuses_cpu_tensors():
     t = torch.zeros((64, 2, 16), dtype=torch.bfloat16)
     with pytest.raises(ValueError):
         L.refresh_attn(p, t, t, t, t)
+
+
+def test_logit_chunks_abi_matches_oracle():
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "logit_examples.json")))
+    for case in gold["chunk_plans"]:
+        assert L.logit_chunks(case["n_logit"], case["max_num_logits"]) == case["plan"]
+    rng = np.random.default_rng(5)
+    for _ in range(100):
+        n, m = int(rng.integers(0, 100000)), int(rng.integers(1, 5000))
+        assert L.logit_chunks(n, m) == O.logit_chunks(n, m)
+    assert L.lib().dllm_logit_chunks(-1, 5, None, 0) == -1
+    assert L.lib().dllm_logit_chunks(10, 0, None, 0) == -1
+    buf = (ctypes.c_int32 * 1)()
+    assert L.lib().dllm_logit_chunks(10, 3, buf, 1) == -1      # 4 chunks do not fit
+
+
+def test_lm_head_validation_without_gpu():
+    so = L.lib()
+    # workspace size: rows x ceil(V / 256) x 8
+    assert L.lm_head_workspace_bytes(2048, 126464, 2048) == 2048 * 494 * 8
+    assert L.lm_head_workspace_bytes(5000, 300, 2048) == 2048 * 2 * 8
+    assert so.dllm_lm_head_workspace_bytes(-1, 10, 10) < 0
+    fake = 1 << 20   # aligned non-null pointers: every call below must fail before any launch
+    assert so.dllm_lm_head_argmax(fake, fake, 16, 100, 512, 16, fake, fake, 1 << 20, None) == -2   # d % 64
+    assert so.dllm_lm_head_argmax(fake, fake, 16, 128, 0, 16, fake, fake, 1 << 20, None) == -1     # vocab
+    assert so.dllm_lm_head_argmax(fake, fake, 16, 128, 512, 16, fake, fake, 8, None) == -1         # workspace
+    assert so.dllm_lm_head_argmax(fake + 4, fake, 16, 128, 512, 16, fake, fake, 1 << 20, None) == -3  # alignment
+    assert so.dllm_lm_head_argmax(None, fake, 16, 128, 512, 16, fake, fake, 1 << 20, None) == -1
+    assert so.dllm_lm_head_argmax(None, None, 0, 128, 512, 16, None, None, 0, None) == 0            # empty: no-op
