@@ -110,8 +110,8 @@ class ClockSampler:
 def cpu_oracle_rate(wl, budget_s: float = 12.0, max_requests: int | None = None):
     """The fp64 oracle as it stands, on a bounded sample of the workload's
     requests (whole requests: Refresh + importance + select + Reuse, all heads;
-    in a mixed batch the reuse-only requests run Reuse alone on the same index
-    lists the GPU arm uses).  Returns (requests/s, requests timed, seconds, threads).
+    in a mixed batch the Refresh requests run Refresh + select and the
+    reuse-only requests run Reuse alone on the same index lists as the GPU arm).  Returns (requests/s, requests timed, seconds, threads).
     For a mixed batch the rate is the batch's request count over the batch time
     extrapolated from the per-kind mean request times of the sample."""
     import torch
@@ -127,7 +127,9 @@ def cpu_oracle_rate(wl, budget_s: float = 12.0, max_requests: int | None = None)
     done, t_total = 0, 0.0
     for kd, reqs in zip(kinds, order):
         t_kind, n_kind = 0.0, 0
-        for b in reqs:
+        # whole passes over the requests until the time budget is spent (C1 has only
+        # 16 requests: a single pass is ~3 s of oracle time)
+        for b in (reqs * 8 if max_requests is None else reqs):
             if max_requests is not None and done >= max_requests:
                 break
             q, K, V, qb = (t.double().numpy() for t in synth.request_tensors(wl, b))
@@ -140,7 +142,9 @@ def cpu_oracle_rate(wl, budget_s: float = 12.0, max_requests: int | None = None)
                 O.attention_dense(q, K, V)
                 raw = O.raw_scores(q[bs:be], K)
                 sel = O.select_batch([raw], [L], [bs], [be], wl.keep_ratio, wl.pool_window)[0]
-            O.attention_with_cache(qb, K, V, bs, be, sel)
+            if not kd or wl.refresh_mask is None:
+                # mixed (C3) batches: Refresh requests stop at select, as on the GPU leg
+                O.attention_with_cache(qb, K, V, bs, be, sel)
             dt = time.perf_counter() - t0
             t_kind += dt
             t_total += dt
@@ -238,10 +242,12 @@ def main():
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
-    # A step runs Refresh -> select -> Reuse for every request, except in a mixed
-    # (burst) batch (C3: refresh_mask), where only the Refresh requests run
-    # Refresh + select + Reuse and the others run Reuse alone with the index
-    # lists of an earlier selection (generated once, outside the timed region).
+    # A step runs Refresh -> select -> Reuse for every request (C1/C2/C4: the whole
+    # hot path over the batch), except in a mixed (burst) batch (C3: refresh_mask,
+    # SURVEY §8(d)): there the Refresh requests run Refresh + select (their block
+    # output is the dense one; the new index lists serve their next Reuse steps)
+    # and the others run Reuse alone with the index lists of an earlier selection
+    # (generated once, outside the timed region).
     def make_part(sub, refresh):
         bt = synth.make_batch(sub)
         pp = lib.Problem(sub.seq_len, sub.blk_start, sub.blk_end, num_heads=sub.num_heads,
@@ -254,7 +260,7 @@ def main():
             flat = np.concatenate([x.reshape(-1) for x in synth.indices(sub, kk)]).astype(np.int32)
             if flat.size:
                 bf.idx[:flat.size].copy_(torch.from_numpy(flat))
-        return {"wl": sub, "batch": bt, "p": pp, "t": tens, "buf": bf, "refresh": refresh}
+        return {"wl": sub, "batch": bt, "p": pp, "t": tens, "buf": bf, "refresh": refresh, "reuse": True}
 
     if wl.refresh_mask is None:
         parts_local = [make_part(wl, True)]
@@ -263,6 +269,8 @@ def main():
         ui = [i for i, m in enumerate(wl.refresh_mask) if not m]
         parts_local = ([make_part(synth.subset(wl, ri), True)] if ri else []) + \
                       ([make_part(synth.subset(wl, ui), False)] if ui else [])
+        for pt in parts_local:
+            pt["reuse"] = not pt["refresh"]
 
     def step(ev=None):
         stream = torch.cuda.current_stream(dev)   # the capture stream while a graph is recorded
@@ -280,8 +288,9 @@ def main():
         if ev is not None:
             ev[2].record(stream)
         for pt in parts_local:
-            q, qb, kc, vc = pt["t"]
-            lib.reuse_sparse_attn(pt["p"], qb, kc, vc, pt["buf"].idx, pt["buf"].out_blk, stream)
+            if pt["reuse"]:
+                q, qb, kc, vc = pt["t"]
+                lib.reuse_sparse_attn(pt["p"], qb, kc, vc, pt["buf"].idx, pt["buf"].out_blk, stream)
         if ev is not None:
             ev[3].record(stream)
 
@@ -361,16 +370,17 @@ def main():
             off += H * kk[b]
             for kv in range(Hk):
                 uniq_rows += len(np.unique(rows_b[kv * g:(kv + 1) * g])) + sub.blk[b]
-        reuse_bytes += uniq_rows * 2 * D * 2 + 2 * blk_rows * H * D * 2 + 4 * total_idx
-        reuse_logical += sum(H * (sub.blk[b] + kk[b]) for b in range(sub.num_requests)) * 2 * D * 2 + \
-            2 * blk_rows * H * D * 2 + 4 * total_idx
+        if pt["reuse"]:
+            reuse_bytes += uniq_rows * 2 * D * 2 + 2 * blk_rows * H * D * 2 + 4 * total_idx
+            reuse_logical += sum(H * (sub.blk[b] + kk[b]) for b in range(sub.num_requests)) * 2 * D * 2 + \
+                2 * blk_rows * H * D * 2 + 4 * total_idx
         if pt["refresh"]:
             flops_refresh += sum(4.0 * H * L * L * D for L in sub.seq_len)
             select_bytes += 4 * H * rows + 4 * total_idx
         total_idx_all += total_idx
         rows_all += rows
     a_ref = flops_refresh / statistics.mean(t_ref) / 1e12 if flops_refresh else 0.0
-    a_reu = reuse_bytes / statistics.mean(t_reu) / 1e9
+    a_reu = reuse_bytes / statistics.mean(t_reu) / 1e9 if reuse_bytes else 0.0
     a_sel = select_bytes / statistics.mean(t_sel) / 1e9 if select_bytes else 0.0
     main_part = parts_local[0]
     buf = main_part["buf"]
@@ -404,8 +414,12 @@ def main():
     h_in, d_in, h_out, d_out = [], [], [], []
     for pt in parts_local:
         bt, tb, (_, tidx, _, _) = pt["batch"], pt["buf"], pt["p"].layout()
-        h_in += [pin(bt.q_blk), pin(bt.k_cache), pin(bt.v_cache)]
-        d_in += pt["t"][1:]
+        h_in += [pin(bt.k_cache), pin(bt.v_cache)]
+        d_in += pt["t"][2:]
+        if pt["reuse"]:
+            h_in.append(pin(bt.q_blk))
+            d_in.append(pt["t"][1])
+            d_out.append(tb.out_blk)
         if pt["refresh"]:
             h_in.append(pin(bt.q))
             d_in.append(pt["t"][0])
@@ -414,7 +428,6 @@ def main():
             # reuse-only requests bring the index lists of their earlier selection
             h_in.append(tb.idx[:max(tidx, 1)].cpu().pin_memory())
             d_in.append(tb.idx[:max(tidx, 1)])
-        d_out.append(tb.out_blk)
     h_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in d_out]
     h2d = sum(t.numel() * t.element_size() for t in h_in)
     d2h = sum(t.numel() * t.element_size() for t in h_out)
@@ -445,8 +458,11 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r, n, t, cores = cpu_oracle_rate(base, budget_s=12.0)
+        what = ("Refresh+importance+select+Reuse" if base.refresh_mask is None else
+                "mixed: Refresh+importance+select for Refresh requests, Reuse for the rest, batch time "
+                "extrapolated from per-kind means")
         cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{n} of {base.num_requests} {base.name} requests (Refresh+importance+select+Reuse, "
+               "sample": f"{n} request passes over the {base.num_requests} {base.name} requests ({what}, "
                          f"all heads, fp64 numpy), {t:.1f} s"}
 
     if rank == 0:
@@ -479,7 +495,7 @@ def main():
             "launch_mode": launch_mode,
             "ms_per_step_eager": 1e3 * total_eager / args.steps,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": sum((3 if pt["refresh"] else 1) * ((pt["wl"].num_requests + 255) // 256)
+            "gpu_launches": sum((2 * pt["refresh"] + pt["reuse"]) * ((pt["wl"].num_requests + 255) // 256)
                                 for pt in parts_local) * args.steps,
             "clocks": clocks,
             "cpu_baseline": cpu,

@@ -147,6 +147,22 @@ DLLM_API int dllm_pack_kv(const dllm_problem *p, const void *k_cache, const void
 DLLM_API int dllm_reuse_packed(const dllm_problem *p, const void *q_blk, const void *k_cache, const void *v_cache,
                                const void *k_pack, const void *v_pack, void *out_blk, void *stream);
 
+/* Single-launch mixed-phase batch (next row N3; the paper's single varlen
+ * dispatch over a packed batch of Refresh and Reuse requests, PAPER.md:366,
+ * 453-456): dllm_refresh_attn over p_refresh (q, out, scores as there) and
+ * dllm_reuse_sparse_attn over p_reuse (q_blk, idx, out_blk as there), both
+ * reading one paged cache (k_cache, v_cache) through their own block tables,
+ * computed by ONE persistent launch whose CTAs are split between the two phases
+ * in proportion to their estimated times.  Results are bit-identical to the two
+ * separate calls.  The problems must agree on H, H_kv, D and page size.  When
+ * one phase is empty, a phase has more than 256 requests, or D != 128, the same
+ * work runs as the two separate launches.  The Reuse requests' idx come from an
+ * earlier selection; dllm_select_heads(p_refresh, scores, ...) may follow on the
+ * same stream.  All pointers DEVICE; returns DLLM_OK or a negative status. */
+DLLM_API int dllm_mixed_attn(const dllm_problem *p_refresh, const void *q, void *out, float *scores,
+                             const dllm_problem *p_reuse, const void *q_blk, const int32_t *idx, void *out_blk,
+                             const void *k_cache, const void *v_cache, void *stream);
+
 /* ---- Logit decomposition (next row N4; §4.3 "Logit
  * Decomposition", §5; SPEC.md:145-165 plan_logit_chunks /
  * chunked_decode).  The LM head in token chunks of at most max_num_logits rows,

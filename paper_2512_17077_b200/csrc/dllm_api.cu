@@ -33,6 +33,10 @@ cudaError_t launch_refresh_mma(const Plan &, const void *, const void *, const v
                                cudaStream_t);
 cudaError_t launch_reuse_ws(const Plan &, const void *, const void *, const void *, const int32_t *, void *,
                             cudaStream_t);
+cudaError_t launch_mixed_tc(const Plan &rplan, const void *q, const void *k, const void *v, void *out, float *scores,
+                            const Plan &uplan, const void *q_blk, const int32_t *idx, void *out_blk, int n_ref,
+                            int grid, cudaStream_t st);
+int num_sms_mixed();
 int64_t lmhead_vocab_tiles(int vocab);
 cudaError_t launch_lmhead_chunk(const void *hidden, const void *weight, int n_tok, int d_model, int vocab, int row0,
                                 int n_rows, int32_t *ids, void *workspace, cudaStream_t st);
@@ -408,6 +412,66 @@ int dllm_check_indices(const dllm_problem *p, const int32_t *idx, int32_t *d_vio
     e = launch_check_indices(pl, idx, d_violations, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "check_indices launch");
   }
+  return ok();
+}
+
+int dllm_mixed_attn(const dllm_problem *p_refresh, const void *q, void *out, float *scores,
+                    const dllm_problem *p_reuse, const void *q_blk, const int32_t *idx, void *out_blk,
+                    const void *k_cache, const void *v_cache, void *stream) {
+  if (!p_refresh || !p_reuse) return fail(DLLM_ERR_INVALID_ARG, "mixed: NULL problem");
+  Layout lr, lu;
+  int st = make_layout(p_refresh, lr);
+  if (st) return st;
+  st = make_layout(p_reuse, lu);
+  if (st) return st;
+  const int Br = p_refresh->num_requests, Bu = p_reuse->num_requests;
+  if (Br > 0 && Bu > 0 &&
+      (p_refresh->num_heads != p_reuse->num_heads || p_refresh->num_kv_heads != p_reuse->num_kv_heads ||
+       p_refresh->head_dim != p_reuse->head_dim || p_refresh->page_size != p_reuse->page_size))
+    return fail(DLLM_ERR_SHAPE, "mixed: the two problems address one paged cache and must agree on H, H_kv, D, page");
+  const bool single = Br > 0 && Bu > 0 && Br <= kMaxReqPerLaunch && Bu <= kMaxReqPerLaunch &&
+                      p_refresh->head_dim == 128 && refresh_impl_env() == 2 && reuse_impl_env() == 2;
+  if (!single) {
+    // not expressible as one launch (a phase is empty, > kMaxReqPerLaunch requests, or
+    // a head dim / A-B override outside the two tcgen05 kernels): the same work as
+    // separate launches, same results
+    st = dllm_refresh_attn(p_refresh, q, k_cache, v_cache, out, scores, stream);
+    if (st) return st;
+    return dllm_reuse_sparse_attn(p_reuse, q_blk, k_cache, v_cache, idx, out_blk, stream);
+  }
+  if (!q || !out || !q_blk || !out_blk || !k_cache || !v_cache)
+    return fail(DLLM_ERR_INVALID_ARG, "mixed: NULL tensor pointer");
+  if (!idx && lu.cu_k[Bu] > 0) return fail(DLLM_ERR_INVALID_ARG, "mixed: idx is NULL");
+  if (!aligned16(q) || !aligned16(out) || !aligned16(q_blk) || !aligned16(out_blk) || !aligned16(k_cache) ||
+      !aligned16(v_cache))
+    return fail(DLLM_ERR_SHAPE, "mixed: bf16 tensors must be 16-byte aligned");
+  if (scores && ((uintptr_t)scores & 3u)) return fail(DLLM_ERR_SHAPE, "mixed: scores must be 4-byte aligned");
+  const bool with_scores = scores != nullptr;
+  static thread_local Plan rp, up;
+  fill_plan(rp, p_refresh, lr.k, 0, Br, lr.cu_L, lr.cu_blk, lr.cu_k, [&](int b) {
+    return refresh_tc2_units(p_refresh->seq_len[b], p_refresh->blk_start[b], p_refresh->blk_end[b],
+                             p_refresh->num_heads, with_scores);
+  });
+  rp.with_scores = with_scores;
+  fill_plan(up, p_reuse, lu.k, 0, Bu, lu.cu_L, lu.cu_blk, lu.cu_k, [&](int b) {
+    return p_reuse->num_heads * ((p_reuse->blk_end[b] - p_reuse->blk_start[b] + 31) / 32);
+  });
+  // split the SMs between the phases in proportion to their estimated times
+  // (Refresh: 4 H L^2 D FLOP at ~1 PFLOP/s; Reuse: H (blk + k) rows of K and V at ~5 TB/s)
+  double t_ref = 0, t_reu = 0;
+  const double H = p_refresh->num_heads, D = p_refresh->head_dim;
+  for (int b = 0; b < Br; ++b) t_ref += 4.0 * H * (double)p_refresh->seq_len[b] * p_refresh->seq_len[b] * D / 1.0e15;
+  for (int b = 0; b < Bu; ++b)
+    t_reu += H * (double)(p_reuse->blk_end[b] - p_reuse->blk_start[b] + lu.k[b]) * 4.0 * D / 5.0e12;
+  const int nsm = num_sms_mixed();
+  int n_ref = (int)(nsm * t_ref / (t_ref + t_reu) + 0.5);
+  n_ref = n_ref < 1 ? 1 : (n_ref > nsm - 1 ? nsm - 1 : n_ref);
+  if (n_ref > rp.total_units) n_ref = rp.total_units;
+  int n_reu = nsm - n_ref;
+  if (n_reu > up.total_units) n_reu = up.total_units;
+  cudaError_t e = launch_mixed_tc(rp, q, k_cache, v_cache, out, scores, up, q_blk, idx, out_blk, n_ref, n_ref + n_reu,
+                                  (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mixed launch");
   return ok();
 }
 

@@ -36,6 +36,7 @@
 #include "common.cuh"
 #include "plan.h"
 #include "tc_ptx.cuh"
+#include "reuse_tc_body.cuh"
 
 #ifdef DLLM_TRACE
 __device__ long long g_trace2[24][512];
@@ -163,12 +164,14 @@ __device__ __forceinline__ void decode_unit(const Plan &pl, const ReqInfo *rs, i
   u.sc1 = pl.with_scores && u.tile1 && (t1 == nreg || (!extra && t1 == u.bs / TBM));
 }
 
+// The kernel body, shared by refresh_tc2_kernel and the single-launch mixed
+// Refresh/Reuse kernel below: CTA `cta` of `ncta` CTAs working on this plan.  The
+// tensor maps are references to __grid_constant__ kernel parameters.
 template <int D>
-__global__ void __launch_bounds__(THREADS, 1)
-refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUtensorMap tm_q,
-                   const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                   const __grid_constant__ CUtensorMap tm_o, __nv_bfloat16 *__restrict__ out,
-                   float *__restrict__ scores) {
+__device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
+                                                 const CUtensorMap &tm_v, const CUtensorMap &tm_o,
+                                                 __nv_bfloat16 *__restrict__ out, float *__restrict__ scores,
+                                                 const int cta, const int ncta) {
   using C = Cfg<D>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
@@ -230,8 +233,8 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
     const uint32_t boxbytes = (uint32_t)boxrows * 128u;
     // the next unit is decoded mid-unit (off the unit-boundary critical path)
     Unit un;
-    if (blockIdx.x < plan.total_units) decode_unit(plan, rs, blockIdx.x, un);
-    for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x, ++ucnt) {
+    if (cta < plan.total_units) decode_unit(plan, rs, cta, un);
+    for (int unit = cta; unit < plan.total_units; unit += ncta, ++ucnt) {
       if (!kNextDecode) decode_unit(plan, rs, unit, un);
       const Unit u = un;
       const int32_t *bt = plan.block_table + (int64_t)u.bt_row * plan.pages_per_req;
@@ -239,7 +242,7 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
         // All CTAs reach their unit boundaries at about the same time, so the next
         // unit's Q tiles and first K/V steps would be requested by every SM at once;
         // warm L2 with them now, spread over this unit's duration.
-        const int nu = unit + gridDim.x;
+        const int nu = unit + ncta;
         if (nu < plan.total_units) {
           Unit v;
           decode_unit(plan, rs, nu, v);
@@ -295,7 +298,7 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
           }
         }
         __syncwarp();
-        if (kNextDecode && j == 0 && unit + (int)gridDim.x < plan.total_units) decode_unit(plan, rs, unit + gridDim.x, un);
+        if (kNextDecode && j == 0 && unit + ncta < plan.total_units) decode_unit(plan, rs, unit + ncta, un);
         if (key_end < TBN) {
           // zero V rows >= key_end (P is 0 there, but 0 * NaN would poison O)
           ptx::mbar_wait(bar((kKVMerged ? B_KFULL : B_VFULL) + s), ph);
@@ -321,11 +324,11 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
     if (lane == 0) {
       int ucnt = 0;
       Unit un;
-      if (blockIdx.x < plan.total_units) decode_unit(plan, rs, blockIdx.x, un);
-      for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x, ++ucnt) {
+      if (cta < plan.total_units) decode_unit(plan, rs, cta, un);
+      for (int unit = cta; unit < plan.total_units; unit += ncta, ++ucnt) {
         if (!kNextDecode) decode_unit(plan, rs, unit, un);
         const Unit u = un;
-        if (kNextDecode && unit + (int)gridDim.x < plan.total_units) decode_unit(plan, rs, unit + gridDim.x, un);
+        if (kNextDecode && unit + ncta < plan.total_units) decode_unit(plan, rs, unit + ncta, un);
         TRACE2(20, ucnt);
         ptx::mbar_wait(bar(B_QEMPTY), (ucnt & 1) ^ 1);
         TRACE2(21, ucnt);
@@ -354,8 +357,8 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
       int gp[2] = {0, 0};        // P.V issued per Q tile
       int ou[2] = {0, 0};        // units per Q tile (O accumulator reuse)
       Unit un;
-      if (blockIdx.x < plan.total_units) decode_unit(plan, rs, blockIdx.x, un);
-      for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x, ++ucnt) {
+      if (cta < plan.total_units) decode_unit(plan, rs, cta, un);
+      for (int unit = cta; unit < plan.total_units; unit += ncta, ++ucnt) {
         if (lane == 0) TRACE2(23, 2 * ucnt);
         if (!kNextDecode) decode_unit(plan, rs, unit, un);
         const Unit u = un;
@@ -400,7 +403,7 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
           if (!kKVMerged) ptx::mma_commit_elect(bar(B_KEMPTY + st));
         }
         if (u.n <= 2) ptx::mma_commit_elect(bar(B_QEMPTY));
-        if (kNextDecode && unit + (int)gridDim.x < plan.total_units) decode_unit(plan, rs, unit + gridDim.x, un);
+        if (kNextDecode && unit + ncta < plan.total_units) decode_unit(plan, rs, unit + ncta, un);
         for (int j = 0; j < u.n; ++j) {
           const int sv = (it + j) % NST;
           if (lane == 0) TRACE2(10, it + j);
@@ -456,7 +459,7 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
     float *sbuf = reinterpret_cast<float *>(gb + C::kOffSc) + wg * (2 * 4 * TBN);
     const float sl2 = plan.scale_log2;
     int sc = 0, oc = 0;
-    for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x) {
+    for (int unit = cta; unit < plan.total_units; unit += ncta) {
       Unit u;
       decode_unit(plan, rs, unit, u);
       if (wg == 1 && !u.tile1) continue;
@@ -603,7 +606,7 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
     uint8_t *stg = gb + C::kOffStage + wq * 32 * 64;
     const uint32_t stg_s = sb + C::kOffStage + wq * 32 * 64;
     int oc[2] = {0, 0};
-    for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x) {
+    for (int unit = cta; unit < plan.total_units; unit += ncta) {
       Unit u;
       decode_unit(plan, rs, unit, u);
       for (int i = 0; i < (u.tile1 ? 2 : 1); ++i) {
@@ -663,7 +666,7 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
   __syncthreads();
   ptx::tc_fence_after();
 #ifdef DLLM_TRACE
-  if (threadIdx.x == 0 && blockIdx.x < 1024) {
+  if (threadIdx.x == 0 && cta < 1024) {
     g_cta2[blockIdx.x][1] = gtimer();
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -672,6 +675,38 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
 #endif
   if (warp == kMmaWarp) ptx::tmem_dealloc(tmem, 512);
 }
+
+template <int D>
+__global__ void __launch_bounds__(THREADS, 1)
+refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUtensorMap tm_q,
+                   const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                   const __grid_constant__ CUtensorMap tm_o, __nv_bfloat16 *__restrict__ out,
+                   float *__restrict__ scores) {
+  refresh_tc2_body<D>(plan, tm_q, tm_k, tm_v, tm_o, out, scores, (int)blockIdx.x, (int)gridDim.x);
+}
+
+// Single-launch mixed-phase batch (the paper's single varlen
+// dispatch over a packed batch of Refresh and Reuse requests, PAPER.md:366,
+// 453-456): CTAs [0, n_ref) run the Refresh body over the Refresh requests'
+// plan, CTAs [n_ref, grid) the Reuse body over the Reuse requests' plan, both
+// persistent, in one launch with the same 512-thread block (the larger of the
+// two shared-memory layouts; each body carves its own).  The tensor-bound and
+// the HBM-bound phase finish together when n_ref follows their estimated times,
+// and there is no kernel boundary between them.
+__global__ void __launch_bounds__(THREADS, 1)
+mixed_tc_kernel(const __grid_constant__ Plan rplan, const __grid_constant__ CUtensorMap tm_q,
+                const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                const __grid_constant__ CUtensorMap tm_o, __nv_bfloat16 *__restrict__ out, float *__restrict__ scores,
+                const __grid_constant__ Plan uplan, const __nv_bfloat16 *__restrict__ q_blk,
+                const __nv_bfloat16 *__restrict__ k_cache, const __nv_bfloat16 *__restrict__ v_cache,
+                const int32_t *__restrict__ idx, __nv_bfloat16 *__restrict__ out_blk, const int n_ref) {
+  if ((int)blockIdx.x < n_ref)
+    refresh_tc2_body<128>(rplan, tm_q, tm_k, tm_v, tm_o, out, scores, (int)blockIdx.x, n_ref);
+  else
+    rtc::reuse_tc_body(uplan, q_blk, k_cache, v_cache, idx, out_blk, (int)blockIdx.x - n_ref,
+                       (int)gridDim.x - n_ref);
+}
+static_assert(THREADS == rtc::kTThreads, "mixed kernel: both bodies run 512-thread CTAs");
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -693,13 +728,12 @@ int num_sms() {
 }
 
 template <int D>
-cudaError_t launch_d(const Plan &plan, const void *q, const void *k, const void *v, void *out, float *scores,
-                     cudaStream_t st) {
+cudaError_t make_maps(const Plan &plan, const void *q, const void *k, const void *v, void *out, CUtensorMap &tq,
+                      CUtensorMap &tk, CUtensorMap &tv, CUtensorMap &to) {
   auto enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
   int64_t rows = 0;
   for (int b = 0; b < plan.nreq; ++b) rows = rows > plan.r[b].q_off + plan.r[b].L ? rows : plan.r[b].q_off + plan.r[b].L;
-  CUtensorMap tq, tk, tv, to;
   {
     cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)plan.H, (cuuint64_t)rows};
     cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)plan.H * D * 2};
@@ -733,6 +767,15 @@ cudaError_t launch_d(const Plan &plan, const void *q, const void *k, const void 
         return cudaErrorInvalidValue;
     }
   }
+  return cudaSuccess;
+}
+
+template <int D>
+cudaError_t launch_d(const Plan &plan, const void *q, const void *k, const void *v, void *out, float *scores,
+                     cudaStream_t st) {
+  CUtensorMap tq, tk, tv, to;
+  cudaError_t me = make_maps<D>(plan, q, k, v, out, tq, tk, tv, to);
+  if (me != cudaSuccess) return me;
   const int smem = Cfg<D>::bytes(plan.nreq);
   cudaError_t e = cudaFuncSetAttribute(refresh_tc2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -743,6 +786,25 @@ cudaError_t launch_d(const Plan &plan, const void *q, const void *k, const void 
 }
 
 }  // namespace
+
+cudaError_t launch_mixed_tc(const Plan &rplan, const void *q, const void *k, const void *v, void *out, float *scores,
+                            const Plan &uplan, const void *q_blk, const int32_t *idx, void *out_blk, int n_ref,
+                            int grid, cudaStream_t st) {
+  if (rplan.D != 128 || uplan.D != 128) return cudaErrorInvalidValue;
+  CUtensorMap tq, tk, tv, to;
+  cudaError_t e = make_maps<128>(rplan, q, k, v, out, tq, tk, tv, to);
+  if (e != cudaSuccess) return e;
+  const int smem = Cfg<128>::bytes(rplan.nreq) > rtc::kTBytes ? Cfg<128>::bytes(rplan.nreq) : rtc::kTBytes;
+  e = cudaFuncSetAttribute(mixed_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  if (grid <= 0) return cudaSuccess;
+  mixed_tc_kernel<<<grid, THREADS, smem, st>>>(rplan, tq, tk, tv, to, (__nv_bfloat16 *)out, scores, uplan,
+                                               (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k,
+                                               (const __nv_bfloat16 *)v, idx, (__nv_bfloat16 *)out_blk, n_ref);
+  return cudaGetLastError();
+}
+
+int num_sms_mixed() { return num_sms(); }
 
 int refresh_tc2_units(int L, int bs, int be, int H, bool with_scores) {
   const int nt = regular_tiles(L) + ((with_scores && straddles(bs, be)) ? 1 : 0);

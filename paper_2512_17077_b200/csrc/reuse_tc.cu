@@ -1,624 +1,29 @@
-// Reuse sparse attention on the 5th-generation tensor cores (tcgen05 + TMEM)
-// (§2.3, Eq. 4; per-head key sets of §4.5).
-//
-// For request b, query head h and the active block's query rows q:
-//   O_b[q,h] = softmax_j(tau Q_blk[q,h].K[j,kv(h)]) V[j,kv(h)],  j in [bs,be) ++ idx(b,h)
-// with K/V gathered in place from the paged cache.
-//
-// Why transposed.  A work unit has only 32 query rows (one block of one head)
-// but hundreds of keys, and tcgen05 needs M = 128 for the simple one-row-per-
-// TMEM-lane accumulator layout.  So the unit is computed transposed, keys in
-// the M dimension:
-//   S^T[128 keys x 32 rows]  = K_chunk[128 x D] . Q^T           (A = K, K-major)
-//   O^T[D=128 x 32 rows]    += V_chunk^T[D x 128] . P^T          (A = V, MN-major;
-//                                                                 B = P^T, K-major)
-// Each softmax thread owns one key of the chunk (its TMEM lane) and the 32
-// query rows (columns); the per-row max / sum over keys are warp transpose-
-// reductions plus a 4-warp exchange through shared memory.  The legacy
-// mma.sync path peaks at ~2 kFLOP/clk/SM on sm_100a (profiles/
-// r01_micro_tmem_mufu_hmma.log), which made the 64-key chunk of reuse_ws
-// math-bound (~0.85 us per chunk, scripts/trace_reuse.py); here the math is
-// a small fraction of the chunk's HBM time.
-//
-// Roles (320 threads, one CTA per SM, persistent over units):
-//   warps 0-3  softmax + epilogue (TMEM lane quarter = warp);
-//   warp 4     translator: position -> physical cache row for every key of
-//              every chunk (block-table lookups, batched);
-//   warps 5-8  loaders: the unit's Q rows and 16-byte cp.async row gathers of
-//              K and V into an NS-stage ring laid out as the UMMA SW128
-//              operand tiles;
-//   warp 9     MMA issuer (one elected lane issues; warp-uniform loop).
-// P^T is written over the stage's K tile once S^T of that chunk is complete,
-// so P needs no shared memory of its own.
-// The data written by cp.async (generic proxy) is published to the tensor
-// core (async proxy) by a proxy fence in the MMA warp after the full barrier.
+// Reuse sparse attention on tcgen05 (Eq. 4; §4.5):
+// the kernel launch around rtc::reuse_tc_body (reuse_tc_body.cuh, where the design
+// is described).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include "common.cuh"
-#include "plan.h"
-#include "tc_ptx.cuh"
+#include "reuse_tc_body.cuh"
+
+#ifdef DLLM_TRACE
+extern "C" __attribute__((visibility("default"))) int dllm_trace_rtc_read(long long *cta, long long *chunk) {
+  cudaError_t e = cudaMemcpyFromSymbol(cta, dllm::rtc::g_rtc, sizeof(dllm::rtc::g_rtc));
+  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(chunk, dllm::rtc::g_rtc_chunk, sizeof(dllm::rtc::g_rtc_chunk));
+  return (int)e;
+}
+#endif
 
 namespace dllm {
 namespace {
 
-constexpr int kTD = 128;            // head dim supported by this kernel
-constexpr int kTRows = 32;          // query rows per unit (MMA N)
-constexpr int kTChunk = 128;        // keys per ring stage (MMA M of S^T)
-#ifndef DLLM_RTC_NS
-#define DLLM_RTC_NS 3
-#endif
-#ifndef DLLM_RTC_DBG
-#define DLLM_RTC_DBG 0   // dev only: 2 = loaders skip the K/V gathers (timing experiments)
-#endif
-#ifndef DLLM_RTC_PMN
-#define DLLM_RTC_PMN 1   // P^T stored MN-major (SW64): 4 x 16-byte stores per thread instead of 32 x 2-byte
-#endif
-#ifndef DLLM_RTC_SLEEP
-#define DLLM_RTC_SLEEP 0   // ns of back-off between polls in the producer-side waits (0: spin)
-#endif
-#ifndef DLLM_RTC_SLEEP_MMA
-#define DLLM_RTC_SLEEP_MMA 0
-#endif
-
-constexpr int kTNS = DLLM_RTC_NS;
-constexpr int kTNT = 4;             // translation ring depth (chunks)
-constexpr int kTTG = 4;             // chunks translated per batch
-// Warp roles (16 warps; the warp schedulers favour the highest warp id among the
-// eligible warps of a sub-partition, so the softmax and epilogue warps sit on top):
-//   0-3, 6-7  loaders         4  translator       5  MMA issuer
-//   8-11      softmax (TMEM lane quarter = warp % 4)
-//   12-15     epilogue: O^T / l -> bf16 rows -> bulk (TMA) stores
-constexpr int kTLoaders = 6, kTransWarp = 4, kMmaWarp = 5, kSoft0 = 8, kEpi0 = 12, kTWarps = 16;
-__device__ __forceinline__ int loader_index(int w) { return w < 4 ? w : (w == 6 || w == 7 ? w - 2 : -1); }
-constexpr int kTThreads = kTWarps * 32;
-
-// shared memory (offsets from a 1024-byte aligned base)
-constexpr int kTileK = kTChunk * kTD * 2;       // 32 KB: [2 atoms][128 rows][128 B]
-constexpr int kStage = 2 * kTileK;              // K then V
-constexpr int kQTile = kTRows * kTD * 2;        // 8 KB: [2 atoms][32 rows][128 B]
-constexpr int kOffQ = kTNS * kStage;
-constexpr int kOffOffs = kOffQ + 2 * kQTile;    // [kTNT][kTChunk] int32
-constexpr int kOffRed = kOffOffs + kTNT * kTChunk * 4;   // [4 warps][32] chunk row maxima
-constexpr int kOffL = kOffRed + 4 * 32 * 4;            // [2 O buffers][4 warps][32 rows] partial row sums
-constexpr int kOffStage = kOffL + 2 * 4 * 32 * 4;      // output staging [32 rows][D] bf16
-constexpr int kBtMax = 1024;                          // block-table entries cached in shared memory
-constexpr int kOffBt = kOffStage + kTRows * kTD * 2;  // [kBtMax] int32
-constexpr int kOffBar = kOffBt + kBtMax * 4;
-constexpr int kNumBars = 2 * kTNS + 2 * kTNT + 2 + 2 + 2 + 2 + 2 + 1 + 2 + 2 + 2 + 1;
-constexpr int kTBytes = kOffBar + 8 * kNumBars + 1024;   // + alignment slack
-static_assert(kTBytes <= 227 * 1024, "reuse_tc shared memory");
-
-// TMEM columns: S^T double buffer (32 each), O^T double buffer (32 each)
-constexpr uint32_t kTmemCols = 128;
-__device__ __forceinline__ uint32_t tm_s(int b) { return (uint32_t)(b * 32); }
-__device__ __forceinline__ uint32_t tm_o(int b) { return (uint32_t)(64 + b * 32); }
-
-#ifdef DLLM_TRACE
-// per-CTA timeline (globaltimer ns): [0] start, [1] translator: first offsets published,
-// [2] MMA: first S issued, [3..10] softmax: end of unit i, [11] end, [12] SM id;
-// CTA 0 per chunk: [0] published, [1] loader issued, [2] S issued, [3] softmax got S,
-// [4] softmax P written, [5] P.V issued
-__device__ long long g_rtc[1024][16];
-__device__ long long g_rtc_chunk[16][64];
-extern "C" __attribute__((visibility("default"))) int dllm_trace_rtc_read(long long *cta, long long *chunk) {
-  cudaError_t e = cudaMemcpyFromSymbol(cta, g_rtc, sizeof(g_rtc));
-  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(chunk, g_rtc_chunk, sizeof(g_rtc_chunk));
-  return (int)e;
-}
-__device__ __forceinline__ long long rtc_timer() {
-  long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define RTC_CTA(slot)                                                          \
-  do {                                                                         \
-    if (lane == 0 && blockIdx.x < 1024) g_rtc[blockIdx.x][slot] = rtc_timer(); \
-  } while (0)
-#define RTC_CHUNK(kind, t)                                                              \
-  do {                                                                                  \
-    if (lane == 0 && blockIdx.x == 0 && (t) < 64) g_rtc_chunk[kind][t] = rtc_timer();   \
-  } while (0)
-#else
-#define RTC_CTA(slot) \
-  do {                \
-  } while (0)
-#define RTC_CHUNK(kind, t) \
-  do {                     \
-  } while (0)
-#endif
-
-// producer-side waits: poll with a short back-off so that idle producers do not
-// flood the shared-memory pipe that the softmax warps' loads / stores queue on
-template <int NSLEEP>
-__device__ __forceinline__ void wait_bo(uint32_t bar, uint32_t parity) {
-  if (NSLEEP == 0) {
-    ptx::mbar_wait(bar, parity);
-  } else {
-    while (!ptx::mbar_try_wait(bar, parity)) __nanosleep(NSLEEP);
-  }
-}
-
-struct TUnit {
-  int b, h, kvh, rg, blk, bs, nk, k, blk_off, bt_row;
-  int64_t idx_off;
-};
-
-__device__ __forceinline__ void tdecode(const Plan &pl, int unit, TUnit &u) {
-  u.b = plan_find(pl, unit);
-  const ReqInfo &R = pl.r[u.b];
-  u.blk = R.be - R.bs;
-  u.bs = R.bs;
-  const int ngroups = (u.blk + kTRows - 1) / kTRows;
-  const int local = unit - R.unit_off;
-  u.h = local / ngroups;
-  u.rg = local - u.h * ngroups;
-  u.kvh = u.h / (pl.H / pl.H_kv);
-  u.k = R.k;
-  u.nk = u.blk + R.k;
-  u.blk_off = R.blk_off;
-  u.bt_row = R.bt_row;
-  u.idx_off = R.idx_off + (int64_t)u.h * R.k;
-}
-
-__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
-}
-
-// byte offset of 16-byte piece c (of a 2*D-byte row) of row r in a SW128 K-major
-// operand tile with `rows` rows: [D/64 atoms][rows][128 B], piece index XOR (r & 7)
-__device__ __forceinline__ uint32_t sw128_off(int rows, int r, int c) {
-  return (uint32_t)((c >> 3) * rows * 128 + r * 128 + (((c & 7) ^ (r & 7)) << 4));
-}
-
-// Warp transpose-reduction of 32 per-lane values x[0..31] (x[n] = this lane's value
-// for row n): returns, in lane j, op over the 32 lanes of x[j].  Destroys x.
-template <bool MAX>
-__device__ __forceinline__ float transpose_reduce32(float (&x)[32], int lane) {
-#pragma unroll
-  for (int w = 16; w >= 1; w >>= 1) {
-    const bool up = (lane & w) != 0;
-#pragma unroll
-    for (int i = 0; i < w; ++i) {
-      const float send = up ? x[i] : x[i + w];
-      const float keep = up ? x[i + w] : x[i];
-      const float r = __shfl_xor_sync(0xffffffffu, send, w);
-      x[i] = MAX ? fmaxf(keep, r) : keep + r;
-    }
-  }
-  return x[0];
-}
+using namespace rtc;
 
 __global__ void __launch_bounds__(kTThreads, 1)
 reuse_tc_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restrict__ q_blk,
                 const __nv_bfloat16 *__restrict__ k_cache, const __nv_bfloat16 *__restrict__ v_cache,
                 const int32_t *__restrict__ idx, __nv_bfloat16 *__restrict__ out) {
-  constexpr int D = kTD;
-  constexpr int CH = D / 8;    // 16-byte pieces per row
-  constexpr int NS = kTNS;
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw = smem_u32(smem_raw);
-  const uint32_t sb = (raw + 1023u) & ~1023u;
-  uint8_t *gb = smem_raw + (sb - raw);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  // barriers
-  const uint32_t b_kvfull = sb + kOffBar;             // [NS] loaders (32*kTLoaders noinc)
-  const uint32_t b_kvempty = b_kvfull + 8 * NS;       // [NS] MMA commit
-  const uint32_t b_ofull_t = b_kvempty + 8 * NS;      // [kTNT] translator (1)
-  const uint32_t b_oempty_t = b_ofull_t + 8 * kTNT;   // [kTNT] loaders (kTLoaders)
-  const uint32_t b_qfull = b_oempty_t + 8 * kTNT;     // [2] loaders (32*kTLoaders noinc)
-  const uint32_t b_qempty = b_qfull + 16;             // [2] MMA commit
-  const uint32_t b_sfull = b_qempty + 16;             // [2] MMA commit
-  const uint32_t b_sfree = b_sfull + 16;              // [2] softmax warps (4)
-  const uint32_t b_pfull = b_sfree + 16;              // [2] softmax warps (4)
-  const uint32_t b_pvdone = b_pfull + 16;             // [1] MMA commit after every P.V
-  const uint32_t b_ofull = b_pvdone + 8;              // [2] MMA commit (unit's last P.V)
-  const uint32_t b_ofree = b_ofull + 16;              // [2] epilogue warps (4): O^T and row sums consumed
-  const uint32_t b_lfull = b_ofree + 16;              // [2] softmax warps (4): row sums written
-  const uint32_t b_tslot = b_lfull + 16;              // TMEM base address slot
-  int32_t *offs = reinterpret_cast<int32_t *>(gb + kOffOffs);
-
-#ifdef DLLM_TRACE
-  if (threadIdx.x == 0 && blockIdx.x < 1024) {
-    for (int i = 0; i < 16; ++i) g_rtc[blockIdx.x][i] = 0;
-    g_rtc[blockIdx.x][0] = rtc_timer();
-    uint32_t smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    g_rtc[blockIdx.x][12] = smid;
-  }
-#endif
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < NS; ++i) {
-      ptx::mbar_init(b_kvfull + 8 * i, 32 * kTLoaders);
-      ptx::mbar_init(b_kvempty + 8 * i, 1);
-    }
-    for (int i = 0; i < kTNT; ++i) {
-      ptx::mbar_init(b_ofull_t + 8 * i, 1);
-      ptx::mbar_init(b_oempty_t + 8 * i, kTLoaders);
-    }
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(b_qfull + 8 * i, 32 * kTLoaders);
-      ptx::mbar_init(b_qempty + 8 * i, 1);
-      ptx::mbar_init(b_sfull + 8 * i, 1);
-      ptx::mbar_init(b_sfree + 8 * i, 4);
-      ptx::mbar_init(b_pfull + 8 * i, 4);
-      ptx::mbar_init(b_ofull + 8 * i, 1);
-      ptx::mbar_init(b_ofree + 8 * i, 4);
-      ptx::mbar_init(b_lfull + 8 * i, 4);
-    }
-    ptx::mbar_init(b_pvdone, 1);
-    ptx::fence_mbar_init();
-  }
-  if (warp == kMmaWarp) {
-    ptx::tmem_alloc(b_tslot, kTmemCols);
-    ptx::tmem_relinquish();
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = *reinterpret_cast<volatile uint32_t *>(gb + (b_tslot - sb));
-
-  if (warp < kSoft0) asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n" ::: "memory");
-  if (warp == kTransWarp) {
-    // ============================ translator (+ Q rows) ============================
-    // every index list and block-table row this CTA will translate, pulled into L2
-    for (int unit = blockIdx.x + lane * gridDim.x; unit < plan.total_units; unit += 32 * gridDim.x) {
-      TUnit u;
-      tdecode(plan, unit, u);
-      if (u.k > 0) {
-        const uintptr_t a0 = reinterpret_cast<uintptr_t>(idx + u.idx_off) & ~uintptr_t(15);
-        const uintptr_t a1 = (reinterpret_cast<uintptr_t>(idx + u.idx_off + u.k) + 15) & ~uintptr_t(15);
-        ptx::bulk_prefetch_l2(reinterpret_cast<const void *>(a0), (uint32_t)(a1 - a0));
-      }
-      const uintptr_t b0 = reinterpret_cast<uintptr_t>(plan.block_table + (int64_t)u.bt_row * plan.pages_per_req) &
-                           ~uintptr_t(15);
-      const uintptr_t b1 =
-          (reinterpret_cast<uintptr_t>(plan.block_table + (int64_t)(u.bt_row + 1) * plan.pages_per_req) + 15) &
-          ~uintptr_t(15);
-      ptx::bulk_prefetch_l2(reinterpret_cast<const void *>(b0), (uint32_t)(b1 - b0));
-    }
-    int t = 0, bt_cached = -1;
-    int *bts = reinterpret_cast<int *>(gb + kOffBt);
-    for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x) {
-      TUnit u;
-      tdecode(plan, unit, u);
-      const int32_t *my_idx = idx + u.idx_off;
-      const int32_t *bt = plan.block_table + (int64_t)u.bt_row * plan.pages_per_req;
-      const int nchunks = (u.nk + kTChunk - 1) / kTChunk;
-      const bool bt_smem = plan.pages_per_req <= kBtMax;
-      for (int g0 = 0; g0 < nchunks; g0 += kTTG) {
-        constexpr int Q = kTTG * kTChunk / 32;
-        int pos[Q], off[Q];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          const int j = g0 * kTChunk + q * 32 + lane;
-          pos[q] = j < u.nk ? (j < u.blk ? u.bs + j : __ldg(my_idx + (j - u.blk))) : -1;
-        }
-        if (g0 == 0 && bt_smem && u.bt_row != bt_cached) {
-          // the request's block-table row goes to shared memory while the index loads
-          // above are in flight: a translation costs one memory round trip, not two
-          __syncwarp();
-          for (int i0 = 0; i0 < plan.pages_per_req; i0 += 8 * 32) {
-            int v[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const int i = i0 + q * 32 + lane;
-              v[q] = i < plan.pages_per_req ? __ldg(bt + i) : 0;
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const int i = i0 + q * 32 + lane;
-              if (i < plan.pages_per_req) bts[i] = v[q];
-            }
-          }
-          bt_cached = u.bt_row;
-        }
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          const int pi = pos[q] >= 0 ? (pos[q] >> plan.page_shift) : 0;
-          const int page = pos[q] >= 0 ? (bt_smem ? bts[pi] : __ldg(bt + pi)) : 0;
-          off[q] = pos[q] >= 0 ? (page * plan.H_kv + u.kvh) * plan.page_size + (pos[q] & (plan.page_size - 1)) : -1;
-        }
-        const int ng = min(kTTG, nchunks - g0);
-#pragma unroll
-        for (int c = 0; c < kTTG; ++c) {
-          if (c >= ng) break;
-          const int slot = t % kTNT;
-          wait_bo<DLLM_RTC_SLEEP>(b_oempty_t + 8 * slot, ((t / kTNT) & 1) ^ 1);
-#pragma unroll
-          for (int rr = 0; rr < kTChunk / 32; ++rr) offs[slot * kTChunk + rr * 32 + lane] = off[c * (kTChunk / 32) + rr];
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(b_ofull_t + 8 * slot);
-          if (t == 0) RTC_CTA(1);
-          RTC_CHUNK(0, t);
-          ++t;
-        }
-      }
-    }
-    cp_async_wait<0>();
-  } else if (loader_index(warp) >= 0) {
-    // ============================ loaders ============================
-    const int li = loader_index(warp);
-    const int64_t HD = (int64_t)plan.H * D;
-    int t = 0, qc = 0;
-    for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x, ++qc) {
-      TUnit u;
-      tdecode(plan, unit, u);
-      const int nchunks = (u.nk + kTChunk - 1) / kTChunk;
-      {
-        // the unit's 32 query rows (zero rows past the block), SW128 K-major
-        const int row0 = u.rg * kTRows;
-        const int qb = qc & 1;
-        wait_bo<DLLM_RTC_SLEEP>(b_qempty + 8 * qb, ((qc >> 1) & 1) ^ 1);
-        const uint32_t sq = sb + kOffQ + qb * kQTile;
-        for (int i = li * 32 + lane; i < kTRows * CH; i += 32 * kTLoaders) {
-          const int r = i / CH, c = i - r * CH;
-          const bool ok = row0 + r < u.blk;
-          const __nv_bfloat16 *src = q_blk + (int64_t)(u.blk_off + (ok ? row0 + r : 0)) * HD + (int64_t)u.h * D + c * 8;
-          cp_async16(sq + sw128_off(kTRows, r, c), src, ok ? 16 : 0);
-        }
-        cp_async_arrive_noinc(b_qfull + 8 * qb);
-      }
-      for (int c = 0; c < nchunks; ++c, ++t) {
-        const int slot = t % kTNT, s = t % NS;
-        wait_bo<DLLM_RTC_SLEEP>(b_ofull_t + 8 * slot, (t / kTNT) & 1);
-        wait_bo<DLLM_RTC_SLEEP>(b_kvempty + 8 * s, ((t / NS) & 1) ^ 1);
-        const uint32_t dk = sb + s * kStage, dv = dk + kTileK;
-#pragma unroll 4
-        for (int e = li * 32 + lane; e < (DLLM_RTC_DBG == 2 ? 0 : kTChunk * CH); e += 32 * kTLoaders) {
-          const int r = e / CH, cc = e - r * CH;
-          const int off = offs[slot * kTChunk + r];
-          const int64_t goff = (int64_t)(off < 0 ? 0 : off) * D + cc * 8;
-          const int nb = off < 0 ? 0 : 16;
-          const uint32_t so = sw128_off(kTChunk, r, cc);
-          cp_async16(dk + so, k_cache + goff, nb);
-          cp_async16(dv + so, v_cache + goff, nb);
-        }
-        cp_async_arrive_noinc(b_kvfull + 8 * s);
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(b_oempty_t + 8 * slot);
-        if (li == 0) RTC_CHUNK(1, t);
-      }
-    }
-    cp_async_wait<0>();
-  } else if (warp == kMmaWarp) {
-    // ============================ MMA issuer ============================
-    constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(128, kTRows, false, false);
-    constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(128, kTRows, true, DLLM_RTC_PMN != 0);
-    const uint64_t dk0 = ptx::smem_desc_sw128(sb, 16, 1024);                 // K tile (K-major) / P^T (K-major)
-    const uint64_t dv0 = ptx::smem_desc_sw128(sb + kTileK, kTChunk * 128, 1024);   // V tile as MN-major A
-    const uint64_t dq0 = ptx::smem_desc_sw128(sb + kOffQ, 16, 1024);
-    // P^T MN-major SW64: one 32-row atom along N, 8-key groups 512 B apart along K
-    const uint64_t dpm0 = ptx::smem_desc(sb, 64 * 8 * 2, 512, ptx::kSwizzle64B);
-    int t = 0, uc = 0;
-    int pv_t = -1, pv_s = 0, pv_ob = 0, pv_first = 0, pv_last = 0, pv_uc = 0;
-    auto issue_pv = [&]() {
-      wait_bo<DLLM_RTC_SLEEP_MMA>(b_pfull + 8 * (pv_t & 1), (pv_t >> 1) & 1);
-      if (pv_first) wait_bo<DLLM_RTC_SLEEP_MMA>(b_ofree + 8 * pv_ob, ((pv_uc >> 1) & 1) ^ 1);
-      ptx::tc_fence_after();
-      const uint64_t a0 = dv0 + (uint64_t)((pv_s * kStage) >> 4);
-      const uint64_t p0 = (DLLM_RTC_PMN ? dpm0 : dk0) + (uint64_t)((pv_s * kStage) >> 4);
-#pragma unroll
-      for (int k = 0; k < kTChunk / 16; ++k) {
-        const uint32_t ao = (uint32_t)((k * 16 * 128) >> 4);
-        const uint32_t bo = DLLM_RTC_PMN ? (uint32_t)((k * 16 * 64) >> 4)
-                                         : (uint32_t)(((k >> 2) * kTRows * 128 + (k & 3) * 32) >> 4);
-        ptx::mma_ss_elect(tmem + tm_o(pv_ob), a0 + ao, p0 + bo, idesc_o, (!pv_first || k > 0) ? 1u : 0u);
-      }
-      ptx::mma_commit_elect(b_kvempty + 8 * pv_s);
-      ptx::mma_commit_elect(b_pvdone);
-      RTC_CHUNK(5, pv_t);
-      if (pv_last) ptx::mma_commit_elect(b_ofull + 8 * pv_ob);
-    };
-    for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x, ++uc) {
-      TUnit u;
-      tdecode(plan, unit, u);
-      const int nchunks = (u.nk + kTChunk - 1) / kTChunk;
-      const int qb = uc & 1;
-      wait_bo<DLLM_RTC_SLEEP_MMA>(b_qfull + 8 * qb, (uc >> 1) & 1);
-      for (int c = 0; c < nchunks; ++c, ++t) {
-        const int s = t % NS, sbuf = t & 1;
-        wait_bo<DLLM_RTC_SLEEP_MMA>(b_kvfull + 8 * s, (t / NS) & 1);
-        wait_bo<DLLM_RTC_SLEEP_MMA>(b_sfree + 8 * sbuf, ((t >> 1) & 1) ^ 1);
-        ptx::fence_proxy_async_smem();   // cp.async (generic proxy) data -> tensor core (async proxy)
-        ptx::tc_fence_after();
-        const uint64_t a0 = dk0 + (uint64_t)((s * kStage) >> 4);
-        const uint64_t b0 = dq0 + (uint64_t)((qb * kQTile) >> 4);
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t ao = (uint32_t)(((k >> 2) * kTChunk * 128 + (k & 3) * 32) >> 4);
-          const uint32_t bo = (uint32_t)(((k >> 2) * kTRows * 128 + (k & 3) * 32) >> 4);
-          ptx::mma_ss_elect(tmem + tm_s(sbuf), a0 + ao, b0 + bo, idesc_s, k > 0 ? 1u : 0u);
-        }
-        ptx::mma_commit_elect(b_sfull + 8 * sbuf);
-        if (t == 0) RTC_CTA(2);
-        RTC_CHUNK(2, t);
-        if (c == nchunks - 1) ptx::mma_commit_elect(b_qempty + 8 * qb);
-        if (pv_t >= 0) issue_pv();
-        pv_t = t; pv_s = s; pv_ob = uc & 1; pv_first = c == 0; pv_last = c == nchunks - 1; pv_uc = uc;
-      }
-      // the unit's last P.V goes out now, not behind the next unit's first K chunk:
-      // the epilogue waits for it
-      issue_pv();
-      pv_t = -1;
-    }
-  } else if (warp < kEpi0) {
-    // ============================ softmax (warps 8-11) ============================
-    // Thread = one key of the chunk (TMEM lane), 32 query rows (columns).  Every
-    // thread keeps the running row maxima m_run[0..31] (identical in all 128
-    // threads).  Common case: no key of the chunk exceeds its row's running max
-    // by more than 2^8 (lazy rescale), decided with one 128-thread barrier-OR,
-    // and the chunk costs one exp2 per score plus four 16-byte P^T stores.
-    // Otherwise the chunk's row maxima are exchanged (redux.sync + shared
-    // memory) and l / O^T are rescaled.
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n" ::: "memory");
-    const int sw = warp & 3;   // TMEM lane quarter
-    const float sl2 = plan.scale_log2;
-    float *red = reinterpret_cast<float *>(gb + kOffRed);   // [4 warps][32] chunk maxima
-    float *lbuf = reinterpret_cast<float *>(gb + kOffL);
-    const uint32_t lane_base = (uint32_t)(sw * 32) << 16;
-    int t = 0, uc = 0;
-    for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x, ++uc) {
-      TUnit u;
-      tdecode(plan, unit, u);
-      const int nchunks = (u.nk + kTChunk - 1) / kTChunk;
-      const int ob = uc & 1;
-      float m_run[32], l_part[32];
-#pragma unroll
-      for (int n = 0; n < 32; ++n) { m_run[n] = -INFINITY; l_part[n] = 0.f; }
-      for (int c = 0; c < nchunks; ++c, ++t) {
-        const int sbuf = t & 1;
-        ptx::mbar_wait(b_sfull + 8 * sbuf, (t >> 1) & 1);
-        ptx::tc_fence_after();
-        if (sw == 0) RTC_CHUNK(3, t);
-        const int key = c * kTChunk + sw * 32 + lane;
-        const bool valid = key < u.nk;
-        float x[32];
-        float dmax = -INFINITY;
-        {
-          uint32_t r[32];
-          DLLM_TMEM_LD32(tmem + lane_base + tm_s(sbuf), r);
-          ptx::tmem_wait_ld();
-#pragma unroll
-          for (int n = 0; n < 32; ++n) {
-            x[n] = valid ? __uint_as_float(r[n]) * sl2 : -INFINITY;
-            dmax = fmaxf(dmax, x[n] - m_run[n]);   // NaN (-inf - -inf) is ignored by fmaxf
-          }
-        }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(b_sfree + 8 * sbuf);
-        const bool rare = ptx::bar_red_or(1, 128, dmax > 8.f);
-        if (sw == 0) RTC_CHUNK(6, t);
-        if (rare) {
-          // chunk row maxima: warp transpose-reduction (lane j <- max of row j over the
-          // warp's 32 keys), the four warps through shared memory, broadcast by shuffles
-          float wmx;
-          {
-            float tmp[32];
-#pragma unroll
-            for (int n = 0; n < 32; ++n) tmp[n] = x[n];
-            wmx = transpose_reduce32<true>(tmp, lane);
-          }
-          red[sw * 32 + lane] = wmx;
-          ptx::named_bar_sync(1, 128);
-          // (the next write of `red` happens after the next barrier-OR, i.e. after every
-          // warp has read it here)
-          const float mc = fmaxf(fmaxf(red[lane], red[32 + lane]), fmaxf(red[64 + lane], red[96 + lane]));
-          float alpha[32];
-#pragma unroll
-          for (int n = 0; n < 32; ++n) {
-            const float mn = fmaxf(m_run[n], __shfl_sync(0xffffffffu, mc, n));
-            alpha[n] = fast_exp2(m_run[n] - mn);
-            m_run[n] = mn;
-            l_part[n] *= alpha[n];
-          }
-          if (c > 0) {
-            // O^T of this unit holds chunks < c: wait for P.V(t-1), rescale its columns
-            ptx::mbar_wait(b_pvdone, (t - 1) & 1);
-            ptx::tc_fence_after();
-#pragma unroll
-            for (int n4 = 0; n4 < 8; ++n4) {
-              uint32_t o4[4];
-              DLLM_TMEM_LD4(tmem + lane_base + tm_o(ob) + 4 * n4, o4);
-              ptx::tmem_wait_ld();
-#pragma unroll
-              for (int e = 0; e < 4; ++e) o4[e] = __float_as_uint(__uint_as_float(o4[e]) * alpha[4 * n4 + e]);
-              DLLM_TMEM_ST4(tmem + lane_base + tm_o(ob) + 4 * n4, o4);
-            }
-            ptx::tmem_wait_st();
-            ptx::tc_fence_before();
-          }
-        }
-        if (sw == 0) RTC_CHUNK(7, t);
-        // P^T over the stage's K tile, MN-major SW64 operand: key kc's 32 row values are
-        // one 64-byte row (4 pieces of 16 B), piece j stored at j ^ ((kc >> 1) & 3)
-        const int kc = sw * 32 + lane;
-        uint8_t *prow = gb + (t % NS) * kStage + kc * 64;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          uint32_t w4[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int n = 8 * j + 2 * q;
-            const uint32_t pp = pack_bf16(fast_exp2(x[n] - m_run[n]), fast_exp2(x[n + 1] - m_run[n + 1]));
-            l_part[n] += __uint_as_float(pp << 16);
-            l_part[n + 1] += __uint_as_float(pp & 0xffff0000u);
-            w4[q] = pp;
-          }
-          *reinterpret_cast<uint4 *>(prow + ((j ^ ((kc >> 1) & 3)) << 4)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-        }
-        if (sw == 0) RTC_CHUNK(8, t);
-        ptx::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(b_pfull + 8 * sbuf);
-        if (sw == 0) RTC_CHUNK(4, t);
-      }
-      // ---- unit end: this warp's partial row sums -> shared memory for the epilogue
-      const float wsum = transpose_reduce32<false>(l_part, lane);
-      ptx::mbar_wait(b_ofree + 8 * ob, ((uc >> 1) & 1) ^ 1);   // unit uc-2's sums consumed
-      lbuf[ob * 128 + sw * 32 + lane] = wsum;
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(b_lfull + 8 * ob);
-      if (sw == 0) RTC_CHUNK(9, uc);
-    }
-  } else {
-    // ============================ epilogue (warps 12-15) ============================
-    // O^T (thread = head-dim lane d, 32 row columns) / l -> bf16 rows in a staging
-    // tile -> one 256-byte bulk (TMA) store per row.  Plain global stores from the
-    // warps on the critical path were measured to queue for microseconds behind
-    // the gather traffic; here they are off the critical path and asynchronous.
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 152;\n" ::: "memory");
-    const int ew = warp & 3;
-    const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
-    const float *lbuf = reinterpret_cast<const float *>(gb + kOffL);
-    int uc = 0;
-    for (int unit = blockIdx.x; unit < plan.total_units; unit += gridDim.x, ++uc) {
-      TUnit u;
-      tdecode(plan, unit, u);
-      const int ob = uc & 1;
-      ptx::mbar_wait(b_lfull + 8 * ob, (uc >> 1) & 1);
-      ptx::mbar_wait(b_ofull + 8 * ob, (uc >> 1) & 1);
-      ptx::tc_fence_after();
-      if (ew == 0) RTC_CHUNK(10, uc);
-      const float lsum = lbuf[ob * 128 + lane] + lbuf[ob * 128 + 32 + lane] + lbuf[ob * 128 + 64 + lane] +
-                         lbuf[ob * 128 + 96 + lane];
-      const float inv = lsum > 0.f ? __frcp_rn(lsum) : 0.f;   // row `lane`
-      uint32_t o[32];
-      DLLM_TMEM_LD32(tmem + lane_base + tm_o(ob), o);
-      ptx::tmem_wait_ld();
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(b_ofree + 8 * ob);
-      if (ew == 0) ptx::bulk_wait_group_read0();   // previous unit's rows left the staging tile
-      ptx::named_bar_sync(2, 128);
-      uint8_t *stg = gb + kOffStage + (ew * 32 + lane) * 2;
-#pragma unroll
-      for (int n = 0; n < 32; ++n)
-        *reinterpret_cast<__nv_bfloat16 *>(stg + n * (D * 2)) =
-            __float2bfloat16_rn(__uint_as_float(o[n]) * __shfl_sync(0xffffffffu, inv, n));
-      ptx::fence_proxy_async_smem();
-      ptx::named_bar_sync(2, 128);
-      const int row0 = u.rg * kTRows;
-      const int nrows = min(kTRows, u.blk - row0);
-      if (ew == 0 && lane < nrows) {
-        ptx::bulk_s2g(out + ((int64_t)(u.blk_off + row0 + lane) * plan.H + u.h) * D, sb + kOffStage + lane * (D * 2),
-                      D * 2);
-        ptx::bulk_commit_group();
-      }
-      if (ew == 0) RTC_CHUNK(11, uc);
-      if (ew == 0 && uc < 8) RTC_CTA(3 + uc);
-    }
-    if (ew == 0) ptx::bulk_wait_group0();
-    if (ew == 0) RTC_CTA(11);
-  }
-
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  if (warp == kMmaWarp) ptx::tmem_dealloc(tmem, kTmemCols);
+  reuse_tc_body(plan, q_blk, k_cache, v_cache, idx, out, (int)blockIdx.x, (int)gridDim.x);
 }
 
 int num_sms_tc() {

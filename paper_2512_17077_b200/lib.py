@@ -27,7 +27,7 @@ DLLM_ERR_K_RANGE = -4
 DLLM_ERR_CUDA = -5
 
 EXPORTED = ("dllm_keep_count", "dllm_index_layout", "dllm_refresh_attn", "dllm_select_heads", "dllm_select_global",
-            "dllm_reuse_sparse_attn", "dllm_pack_kv", "dllm_reuse_packed", "dllm_logit_chunks",
+            "dllm_reuse_sparse_attn", "dllm_pack_kv", "dllm_reuse_packed", "dllm_mixed_attn", "dllm_logit_chunks",
             "dllm_lm_head_workspace_bytes", "dllm_lm_head_argmax", "dllm_check_indices", "dllm_status_string",
             "dllm_last_error", "dllm_version")
 
@@ -80,6 +80,8 @@ def _load() -> ctypes.CDLL:
     lib.dllm_pack_kv.restype = ctypes.c_int
     lib.dllm_reuse_packed.argtypes = [P, vp, vp, vp, vp, vp, vp, vp]
     lib.dllm_reuse_packed.restype = ctypes.c_int
+    lib.dllm_mixed_attn.argtypes = [P, vp, vp, vp, P, vp, vp, vp, vp, vp, vp]
+    lib.dllm_mixed_attn.restype = ctypes.c_int
     lib.dllm_logit_chunks.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.c_int32]
     lib.dllm_logit_chunks.restype = ctypes.c_int
     lib.dllm_lm_head_workspace_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
@@ -167,6 +169,10 @@ class Problem:
         return ctypes.byref(self._s)
 
     @property
+    def num_requests(self) -> int:
+        return self._s.num_requests
+
+    @property
     def num_heads(self) -> int:
         return self._s.num_heads
 
@@ -244,6 +250,16 @@ def reuse_packed(p: Problem, q_blk, k_cache, v_cache, k_pack, v_pack, out_blk, s
     _check(_lib.dllm_reuse_packed(p.ref, _dev(q_blk, "q_blk", bf), _dev(k_cache, "k_cache", bf),
                                   _dev(v_cache, "v_cache", bf), _dev(k_pack, "k_pack", bf), _dev(v_pack, "v_pack", bf),
                                   _dev(out_blk, "out_blk", bf), _stream(stream)), "dllm_reuse_packed")
+
+
+def mixed_attn(p_refresh: Problem, q, out, scores, p_reuse: Problem, q_blk, idx, out_blk, k_cache, v_cache,
+               stream=None) -> None:
+    """Refresh over p_refresh and Reuse over p_reuse in one launch (N3)."""
+    bf = torch.bfloat16
+    _check(_lib.dllm_mixed_attn(p_refresh.ref, _dev(q, "q", bf), _dev(out, "out", bf),
+                                _dev(scores, "scores", torch.float32), p_reuse.ref, _dev(q_blk, "q_blk", bf),
+                                _dev(idx, "idx", torch.int32), _dev(out_blk, "out_blk", bf), _dev(k_cache, "k_cache", bf),
+                                _dev(v_cache, "v_cache", bf), _stream(stream)), "dllm_mixed_attn")
 
 
 def logit_chunks(n_logit: int, max_num_logits: int) -> list:
