@@ -212,6 +212,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph replay")
+    ap.add_argument("--no-mixed", action="store_true",
+                    help="C3: separate Refresh and Reuse launches instead of one mixed launch")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -262,18 +264,60 @@ def main():
                 bf.idx[:flat.size].copy_(torch.from_numpy(flat))
         return {"wl": sub, "batch": bt, "p": pp, "t": tens, "buf": bf, "refresh": refresh, "reuse": True}
 
+    def make_part_shared(shared, dk, dv, reqs, refresh):
+        # a phase of a mixed batch: its own problem (block-table rows of its requests)
+        # over the batch's ONE paged cache
+        sub = synth.subset(wl, reqs)
+        pp = lib.Problem(sub.seq_len, sub.blk_start, sub.blk_end, num_heads=sub.num_heads,
+                         num_kv_heads=sub.num_kv_heads, head_dim=sub.head_dim, keep_ratio=sub.keep_ratio,
+                         pool_window=sub.pool_window, page_size=sub.page_size,
+                         block_table=shared.block_table[reqs].contiguous().to(dev))
+        q = torch.cat([shared.q_req(b) for b in reqs])
+        qb = torch.cat([shared.q_blk_req(b) for b in reqs])
+        bf = lib.alloc_buffers(pp, device=dev)
+        if not refresh:
+            kk = pp.layout()[0]
+            flat = np.concatenate([x.reshape(-1) for x in synth.indices(sub, kk)]).astype(np.int32)
+            if flat.size:
+                bf.idx[:flat.size].copy_(torch.from_numpy(flat))
+        host = {"q": q, "q_blk": qb, "k_cache": shared.k_cache, "v_cache": shared.v_cache}
+        return {"wl": sub, "host": host, "p": pp, "t": [q.to(dev), qb.to(dev), dk, dv], "buf": bf,
+                "refresh": refresh, "reuse": not refresh}
+
+    mixed = False
     if wl.refresh_mask is None:
         parts_local = [make_part(wl, True)]
     else:
         ri = [i for i, m in enumerate(wl.refresh_mask) if m]
         ui = [i for i, m in enumerate(wl.refresh_mask) if not m]
-        parts_local = ([make_part(synth.subset(wl, ri), True)] if ri else []) + \
-                      ([make_part(synth.subset(wl, ui), False)] if ui else [])
-        for pt in parts_local:
-            pt["reuse"] = not pt["refresh"]
+        shared = synth.make_batch(wl)
+        dk, dv = shared.k_cache.to(dev), shared.v_cache.to(dev)
+        parts_local = ([make_part_shared(shared, dk, dv, ri, True)] if ri else []) + \
+                      ([make_part_shared(shared, dk, dv, ui, False)] if ui else [])
+        # both phases in ONE launch (dllm_mixed_attn, next row N3) unless disabled
+        mixed = len(parts_local) == 2 and not args.no_mixed
+    for pt in parts_local:
+        if "host" not in pt:
+            bt = pt["batch"]
+            pt["host"] = {"q": bt.q, "q_blk": bt.q_blk, "k_cache": bt.k_cache, "v_cache": bt.v_cache}
 
     def step(ev=None):
         stream = torch.cuda.current_stream(dev)   # the capture stream while a graph is recorded
+        if mixed:
+            pr, pu = parts_local
+            q, _, kc, vc = pr["t"]
+            qb = pu["t"][1]
+            if ev is not None:
+                ev[0].record(stream)
+            lib.mixed_attn(pr["p"], q, pr["buf"].out, pr["buf"].scores, pu["p"], qb, pu["buf"].idx, pu["buf"].out_blk,
+                           kc, vc, stream)
+            if ev is not None:
+                ev[1].record(stream)
+            lib.select_heads(pr["p"], pr["buf"].scores, pr["buf"].idx, stream)
+            if ev is not None:
+                ev[2].record(stream)
+                ev[3].record(stream)
+            return
         if ev is not None:
             ev[0].record(stream)
         for pt in parts_local:
@@ -380,11 +424,10 @@ def main():
         total_idx_all += total_idx
         rows_all += rows
     a_ref = flops_refresh / statistics.mean(t_ref) / 1e12 if flops_refresh else 0.0
-    a_reu = reuse_bytes / statistics.mean(t_reu) / 1e9 if reuse_bytes else 0.0
+    a_reu = reuse_bytes / statistics.mean(t_reu) / 1e9 if reuse_bytes and not mixed else 0.0
     a_sel = select_bytes / statistics.mean(t_sel) / 1e9 if select_bytes else 0.0
     main_part = parts_local[0]
     buf = main_part["buf"]
-    batch = main_part["batch"]
     q, qb, kc, vc = main_part["t"]
     p = main_part["p"]
     k, total_idx, rows, blk_rows = p.layout()
@@ -412,17 +455,23 @@ def main():
     # ---- end to end through the public API with host buffers
     pin = lambda t: t.pin_memory()  # noqa: E731
     h_in, d_in, h_out, d_out = [], [], [], []
+    seen = set()
+
+    def add_in(host, dev_t):
+        if id(dev_t) not in seen:    # a mixed batch's phases share one cache: copied once
+            seen.add(id(dev_t))
+            h_in.append(pin(host))
+            d_in.append(dev_t)
+
     for pt in parts_local:
-        bt, tb, (_, tidx, _, _) = pt["batch"], pt["buf"], pt["p"].layout()
-        h_in += [pin(bt.k_cache), pin(bt.v_cache)]
-        d_in += pt["t"][2:]
+        ht, tb, (_, tidx, _, _) = pt["host"], pt["buf"], pt["p"].layout()
+        add_in(ht["k_cache"], pt["t"][2])
+        add_in(ht["v_cache"], pt["t"][3])
         if pt["reuse"]:
-            h_in.append(pin(bt.q_blk))
-            d_in.append(pt["t"][1])
+            add_in(ht["q_blk"], pt["t"][1])
             d_out.append(tb.out_blk)
         if pt["refresh"]:
-            h_in.append(pin(bt.q))
-            d_in.append(pt["t"][0])
+            add_in(ht["q"], pt["t"][0])
             d_out += [tb.out, tb.idx[:max(tidx, 1)]]
         else:
             # reuse-only requests bring the index lists of their earlier selection
@@ -476,11 +525,23 @@ def main():
                        "parallelism": f"request-sharded dp{world} (LPT), no data-path collective",
                        "l2": "flushed before every step (512 MiB write, outside the step events)",
                        "seed": synth.base_seed()},
-            "roofline": {"bound": "tensor", "kernel": "dllm_refresh_attn (tcgen05)", "achieved": a_ref,
-                         "peak": tf_peak, "unit": "TFLOP/s", "frac": a_ref / tf_peak, "traffic": traffic,
-                         "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
-                         "frac_of_sustained": (a_ref / tf_sust) if tf_sust else None},
-            "kernels": {
+            "roofline": ({"bound": "tensor", "kernel": "dllm_refresh_attn (tcgen05)", "achieved": a_ref,
+                          "peak": tf_peak, "unit": "TFLOP/s", "frac": a_ref / tf_peak, "traffic": traffic,
+                          "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
+                          "frac_of_sustained": (a_ref / tf_sust) if tf_sust else None} if not mixed else
+                         {"bound": "tensor+hbm", "kernel": "dllm_mixed_attn (Refresh + Reuse, one launch)",
+                          "achieved": a_ref, "peak": tf_peak, "unit": "TFLOP/s (Refresh FLOP / launch time)",
+                          "frac": (flops_refresh / (tf_peak * 1e12) + reuse_bytes / (hbm_peak * 1e9))
+                          / statistics.mean(t_ref),
+                          "frac_definition": "additive roofline time (Refresh FLOP / bf16 peak + Reuse unique "
+                                             "bytes / HBM peak) / measured launch time", "traffic": None,
+                          "peak_source": f"{peak_src} (MEASURED_PEAKS.json)"}),
+            "kernels": ({
+                "mixed": {"us": 1e6 * statistics.mean(t_ref), "refresh_flop": flops_refresh,
+                          "reuse_bytes_unique": reuse_bytes, "reuse_bytes_logical": reuse_logical,
+                          "roofline_us": 1e6 * (flops_refresh / (tf_peak * 1e12) + reuse_bytes / (hbm_peak * 1e9))},
+                "select": {"us": 1e6 * statistics.mean(t_sel), "GB/s": a_sel, "frac": a_sel / hbm_peak,
+                           "bytes_per_launch": select_bytes}} if mixed else {
                 "refresh": {"us": 1e6 * statistics.mean(t_ref), "TFLOP/s": a_ref, "frac": a_ref / tf_peak,
                             "flop_per_launch": flops_refresh},
                 "select": {"us": 1e6 * statistics.mean(t_sel), "GB/s": a_sel, "frac": a_sel / hbm_peak,
@@ -491,12 +552,12 @@ def main():
                           "peak": hbm_peak},
                 "block_cycle_us": (1e6 * (statistics.mean(t_ref) + statistics.mean(t_sel) + 31 * statistics.mean(t_reu))
                                    if len(parts_local) == 1 and parts_local[0]["refresh"] else None),
-            },
+            }),
             "launch_mode": launch_mode,
             "ms_per_step_eager": 1e3 * total_eager / args.steps,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": sum((2 * pt["refresh"] + pt["reuse"]) * ((pt["wl"].num_requests + 255) // 256)
-                                for pt in parts_local) * args.steps,
+            "gpu_launches": (2 if mixed else sum((2 * pt["refresh"] + pt["reuse"]) * ((pt["wl"].num_requests + 255) // 256)
+                                                 for pt in parts_local)) * args.steps,
             "clocks": clocks,
             "cpu_baseline": cpu,
             "allgather_ms": allgather_ms,
