@@ -539,8 +539,9 @@ const char *dllm_status_string(int status) {
 const char *dllm_last_error(void) { return g_last_error.c_str(); }
 
 const char *dllm_version(void) {
-  return "libdllm sm_100a: refresh=tcgen05/TMEM+TMA (mma.sync fallback for D<64), select=radix-topk, "
-         "reuse=paged-gather cp.async + mma.sync";
+  return "libdllm sm_100a: refresh=tcgen05/TMEM+TMA (mma.sync for D<64), select=radix-topk, "
+         "reuse=paged cp.async gather + tcgen05 (D=128; mma.sync otherwise), mixed=one-launch Refresh+Reuse, "
+         "lm_head=tcgen05 GEMM + fused argmax";
 }
 
 }  // extern "C"
