@@ -17,7 +17,7 @@ buf = lib.alloc_buffers(p)
 for _ in range(3):
     lib.refresh_attn(p, q, kc, vc, buf.out, buf.scores)
 torch.cuda.synchronize()
-tr = np.zeros((24, 512), dtype=np.int64)
+tr = np.zeros((28, 512), dtype=np.int64)
 lib.lib().dllm_trace2_read(tr.ctypes.data_as(ctypes.c_void_p))
 t0 = tr[0, 0]
 names = ["s0wait", "s1wait", "s0gotS", "s1gotS", "s0P", "s1P", "mWaitP0", "mGotP0", "mWaitP1", "mGotP1",
@@ -70,3 +70,7 @@ print("slowest CTAs (cta, smid, us):", [(int(c), int(g[c, 3]), round(dur[c] / 1e
 print("fastest CTAs:", [(int(c), int(g[c, 3]), round(dur[c] / 1e3, 1)) for c in order[-6:]])
 hist = np.histogram(dur / 1e3, bins=10)
 print("hist", [int(x) for x in hist[0]], [round(float(x), 0) for x in hist[1]])
+
+print("producer per step around the first two boundaries (abs - t0): K wait start, K got, V wait start, V got")
+for i in list(range(n_unit - 5, n_unit + 3)) + list(range(2 * n_unit - 3, 2 * n_unit + 2)):
+    print(f"{i:4d} " + " ".join(f"{(tr[k, i] - t0):8d}" for k in (24, 25, 26, 27)))
