@@ -65,11 +65,17 @@ def workload_desc(wl, n):
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """SM clocks and throttle reasons sampled (NVML, every 10 ms) during the timed region."""
+    """SM clocks, power and throttle reasons sampled through NVML every ~2 ms while
+    the timed region runs (samples taken before the region starts are dropped).
+    The timed region of a default run is only a few ms, so `extend(fn, seconds)`
+    keeps replaying the same step afterwards, untimed, and records the clocks the
+    workload settles at under the power cap (reported separately)."""
 
     def __init__(self, index: int):
         self.index, self.samples, self._stop = index, [], threading.Event()
+        self._phase = None
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._ready = threading.Event()
 
     def _run(self):
         try:
@@ -81,29 +87,64 @@ class ClockSampler:
                      "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
                      "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
                      "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            self._ready.set()
             while not self._stop.is_set():
-                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((sm, mx, sorted(k for k, v in names.items() if rs & v)))
-                self._stop.wait(0.01)
+                ph = self._phase
+                if ph is not None:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    try:
+                        pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+                    except Exception:
+                        pw = None
+                    self.samples.append((ph, sm, mx, sorted(k for k, v in names.items() if rs & v), pw))
+                self._stop.wait(0.002)
         except Exception as e:  # pragma: no cover
-            self.samples.append((None, None, [f"nvml-error: {e}"]))
+            self.samples.append(("region", None, None, [f"nvml-error: {e}"], None))
+            self._ready.set()
 
     def __enter__(self):
         self._t.start()
-        time.sleep(0.05)
+        self._ready.wait(timeout=30)
+        self._phase = "region"
         return self
 
     def __exit__(self, *a):
+        self._phase = None
+
+    def extend(self, fn, seconds: float = 0.2):
+        """Replay `fn` (one untimed step, device-synchronised by the caller's loop)
+        for about `seconds` with sampling on, then stop the sampler."""
+        import torch
+        self._phase = "extended"
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < seconds:
+            fn()
+            torch.cuda.synchronize()
+        self._phase = None
         self._stop.set()
         self._t.join(timeout=10)
 
-    def summary(self):
-        sm = [s[0] for s in self.samples if s[0] is not None]
-        mx = [s[1] for s in self.samples if s[1] is not None]
-        reasons = sorted({r for s in self.samples for r in s[2]})
+    def close(self):
+        self._phase = None
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    @staticmethod
+    def _summ(rows):
+        sm = [r[1] for r in rows if r[1] is not None]
+        mx = [r[2] for r in rows if r[2] is not None]
+        pw = [r[4] for r in rows if r[4] is not None]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": sorted({x for r in rows for x in r[3]}), "samples": len(rows),
+                "power_w": statistics.median(pw) if pw else None}
+
+    def summary(self):
+        out = self._summ([r for r in self.samples if r[0] == "region"])
+        ext = [r for r in self.samples if r[0] == "extended"]
+        if ext:
+            out["under_load_extended"] = self._summ(ext)
+        return out
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) timing
@@ -346,11 +387,13 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(local_rank) as clk:
+    clk = ClockSampler(local_rank)
+    with clk:
         for i in range(args.steps):
             flush.zero_()
             step(evs[i])
         torch.cuda.synchronize(dev)
+    clk.close()
     if world > 1:
         dist.barrier()
     t_ref = [evs[i][0].elapsed_time(evs[i][1]) * 1e-3 for i in range(args.steps)]
@@ -380,13 +423,15 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
-        with ClockSampler(local_rank) as clk:
+        clk = ClockSampler(local_rank)
+        with clk:
             for i in range(args.steps):
                 flush.zero_()
                 gev[i][0].record(stream)
                 g.replay()
                 gev[i][1].record(stream)
             torch.cuda.synchronize(dev)
+        clk.extend(g.replay, 0.25)
         if world > 1:
             dist.barrier()
         total = sum(gev[i][0].elapsed_time(gev[i][1]) * 1e-3 for i in range(args.steps))
