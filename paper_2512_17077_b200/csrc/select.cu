@@ -21,8 +21,12 @@
 
 namespace dllm {
 
-constexpr int kSelThreads = 512;
+#ifndef DLLM_SEL_THREADS
+#define DLLM_SEL_THREADS 512
+#endif
+constexpr int kSelThreads = DLLM_SEL_THREADS;
 constexpr int kSelWarps = kSelThreads / 32;
+constexpr int kSelSmemStageMax = 24576;   // words of dynamic smem for staged raw scores + keys (96 KB)
 
 __device__ __forceinline__ uint32_t order_key(float f) {
   uint32_t u = __float_as_uint(f);
@@ -79,15 +83,31 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
   int32_t *out = idx + R.idx_off + (int64_t)h * k;
   const int half = plan.window >> 1;
 
-  // 1. pool on the compacted axis, to order keys
-  for (int c = threadIdx.x; c < n; c += kSelThreads) {
-    const int lo = max(0, c - half), hi = min(n - 1, c + half);
-    float m = -INFINITY;
-    for (int j = lo; j <= hi; ++j) {
-      const int pos = j < bs ? j : j + blk;
-      m = fmaxf(m, __ldg(raw + pos));
+  // 1. pool on the compacted axis, to order keys.  When the candidates fit twice in
+  // shared memory, the raw scores are first staged there with all loads of a thread
+  // in flight together (one memory round trip instead of one per window element and
+  // candidate), then pooled from shared memory.
+  if (2 * n <= kSelSmemStageMax) {
+    float *rawc = reinterpret_cast<float *>(keys + n);
+#pragma unroll 4
+    for (int c = threadIdx.x; c < n; c += kSelThreads) rawc[c] = __ldg(raw + (c < bs ? c : c + blk));
+    __syncthreads();
+    for (int c = threadIdx.x; c < n; c += kSelThreads) {
+      const int lo = max(0, c - half), hi = min(n - 1, c + half);
+      float m = -INFINITY;
+      for (int j = lo; j <= hi; ++j) m = fmaxf(m, rawc[j]);
+      keys[c] = order_key(m);
     }
-    keys[c] = order_key(m);
+  } else {
+    for (int c = threadIdx.x; c < n; c += kSelThreads) {
+      const int lo = max(0, c - half), hi = min(n - 1, c + half);
+      float m = -INFINITY;
+      for (int j = lo; j <= hi; ++j) {
+        const int pos = j < bs ? j : j + blk;
+        m = fmaxf(m, __ldg(raw + pos));
+      }
+      keys[c] = order_key(m);
+    }
   }
   if (threadIdx.x == 0) { s_prefix = 0u; s_krem = k; }
   __syncthreads();
@@ -99,9 +119,15 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int i = threadIdx.x; i < 256; i += kSelThreads) hist[i] = 0;
     __syncthreads();
-    for (int c = threadIdx.x; c < n; c += kSelThreads) {
-      const uint32_t key = keys[c];
-      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 0xffu], 1);
+    // warp-aggregated: the candidates' keys crowd a few bins (similar exponents), so
+    // lanes with equal bins are merged (match.any) into one shared atomic
+    for (int c0 = 0; c0 < n; c0 += kSelThreads) {
+      const int c = c0 + threadIdx.x;
+      const uint32_t key = c < n ? keys[c] : 0u;
+      const bool act = c < n && (key & mask) == prefix;
+      const uint32_t bin = act ? ((key >> shift) & 0xffu) : 0x100u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+      if (act && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -143,20 +169,21 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
   const int need_eq = krem;      // how many keys equal to thr are taken (lowest index first)
 
   // 3. compaction in ascending candidate order
-  int eq_base = 0, out_base = 0;
+  // One block scan per 512 candidates of the packed pair (above, equal): a selected
+  // candidate's output slot is (#above before it) + min(#equal before it, need_eq),
+  // because exactly the first need_eq equal keys are taken.
+  int eq_base = 0, gt_base = 0;
   for (int c0 = 0; c0 < n; c0 += kSelThreads) {
     const int c = c0 + threadIdx.x;
     uint32_t key = c < n ? keys[c] : 0u;
     const int gt = (c < n) && key > thr;
     const int eq = (c < n) && key == thr;
-    int eq_tot;
-    const int eq_rank = eq_base + block_excl_scan(eq, warp_buf, &eq_tot);
-    const int sel = gt || (eq && eq_rank < need_eq);
-    int sel_tot;
-    const int pos_out = out_base + block_excl_scan(sel, warp_buf, &sel_tot);
-    if (sel) out[pos_out] = c < bs ? c : c + blk;
-    eq_base += eq_tot;
-    out_base += sel_tot;
+    int tot;
+    const int pre = block_excl_scan(gt | (eq << 16), warp_buf, &tot);
+    const int gt_pre = gt_base + (pre & 0xffff), eq_pre = eq_base + (pre >> 16);
+    if (gt || (eq && eq_pre < need_eq)) out[gt_pre + min(eq_pre, need_eq)] = c < bs ? c : c + blk;
+    gt_base += tot & 0xffff;
+    eq_base += tot >> 16;
   }
 }
 
@@ -200,9 +227,15 @@ select_global_kernel(const __grid_constant__ Plan plan, const float *__restrict_
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int i = threadIdx.x; i < 256; i += kSelThreads) hist[i] = 0;
     __syncthreads();
-    for (int c = threadIdx.x; c < n; c += kSelThreads) {
-      const uint32_t key = keys[c];
-      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 0xffu], 1);
+    // warp-aggregated: the candidates' keys crowd a few bins (similar exponents), so
+    // lanes with equal bins are merged (match.any) into one shared atomic
+    for (int c0 = 0; c0 < n; c0 += kSelThreads) {
+      const int c = c0 + threadIdx.x;
+      const uint32_t key = c < n ? keys[c] : 0u;
+      const bool act = c < n && (key & mask) == prefix;
+      const uint32_t bin = act ? ((key >> shift) & 0xffu) : 0x100u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+      if (act && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -237,24 +270,23 @@ select_global_kernel(const __grid_constant__ Plan plan, const float *__restrict_
     mask |= 0xffu << shift;
     __syncthreads();
   }
-  int eq_base = 0, out_base = 0;
+  int eq_base = 0, gt_base = 0;
   int32_t *out0 = idx + R.idx_off;
   for (int c0 = 0; c0 < n; c0 += kSelThreads) {
     const int c = c0 + threadIdx.x;
     const uint32_t key = c < n ? keys[c] : 0u;
     const int gt = (c < n) && key > prefix;
     const int eq = (c < n) && key == prefix;
-    int eq_tot;
-    const int eq_rank = eq_base + block_excl_scan(eq, warp_buf, &eq_tot);
-    const int sel = gt || (eq && eq_rank < krem);
-    int sel_tot;
-    const int pos_out = out_base + block_excl_scan(sel, warp_buf, &sel_tot);
-    if (sel) {
+    int tot;
+    const int pre = block_excl_scan(gt | (eq << 16), warp_buf, &tot);
+    const int gt_pre = gt_base + (pre & 0xffff), eq_pre = eq_base + (pre >> 16);
+    if (gt || (eq && eq_pre < krem)) {
       const int pos = c < bs ? c : c + blk;
+      const int pos_out = gt_pre + min(eq_pre, krem);
       for (int h = 0; h < H; ++h) out0[(int64_t)h * k + pos_out] = pos;
     }
-    eq_base += eq_tot;
-    out_base += sel_tot;
+    gt_base += tot & 0xffff;
+    eq_base += tot >> 16;
   }
 }
 
@@ -279,7 +311,8 @@ __global__ void check_indices_kernel(const __grid_constant__ Plan plan, const in
 cudaError_t launch_select(const Plan &plan, const float *scores, int32_t *idx, cudaStream_t st) {
   int max_n = 0;
   for (int b = 0; b < plan.nreq; ++b) max_n = max(max_n, plan.r[b].L - (plan.r[b].be - plan.r[b].bs));
-  const size_t smem = (size_t)max(max_n, 1) * sizeof(uint32_t);
+  const size_t words = 2 * max_n <= kSelSmemStageMax ? 2 * (size_t)max_n : (size_t)max_n;
+  const size_t smem = (words > 0 ? words : 1) * sizeof(uint32_t);
   cudaError_t e = cudaFuncSetAttribute(select_heads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
