@@ -1,6 +1,8 @@
 // Device helpers shared by the kernels (PTX wrappers; no method arithmetic).
 #pragma once
+#include <cstdlib>
 #include <cuda_bf16.h>
+#include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace dllm {
@@ -115,6 +117,45 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
   constexpr int C = D / 8;                      // chunks per row
   constexpr int M = C >= 8 ? 7 : C - 1;         // xor mask within the row
   return (uint32_t)(row * D * 2 + ((chunk ^ (row & M)) << 4));
+}
+
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Kernels of the hot path are launched with programmatic stream serialisation
+// (cudaLaunchAttributeProgrammaticStreamSerialization) so that a kernel's launch
+// and CTA rasterisation overlap the tail of its predecessor on the stream; every
+// such kernel starts with griddepcontrol.wait (a no-op when it was not launched
+// that way), so nothing reads or writes global memory before the predecessor's
+// results are visible, then allows its own successor to launch.
+// DLLM_PDL=0 turns the attribute off (A/B).
+__device__ __forceinline__ void pdl_wait_then_trigger() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *s = getenv("DLLM_PDL");
+    v = (s && s[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
 }  // namespace dllm

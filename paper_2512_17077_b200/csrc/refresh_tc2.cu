@@ -729,6 +729,7 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
                    const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                    const __grid_constant__ CUtensorMap tm_o, __nv_bfloat16 *__restrict__ out,
                    float *__restrict__ scores) {
+  pdl_wait_then_trigger();
   refresh_tc2_body<D>(plan, tm_q, tm_k, tm_v, tm_o, out, scores, (int)blockIdx.x, (int)gridDim.x);
 }
 
@@ -747,6 +748,7 @@ mixed_tc_kernel(const __grid_constant__ Plan rplan, const __grid_constant__ CUte
                 const __grid_constant__ Plan uplan, const __nv_bfloat16 *__restrict__ q_blk,
                 const __nv_bfloat16 *__restrict__ k_cache, const __nv_bfloat16 *__restrict__ v_cache,
                 const int32_t *__restrict__ idx, __nv_bfloat16 *__restrict__ out_blk, const int n_ref) {
+  pdl_wait_then_trigger();
   if ((int)blockIdx.x < n_ref)
     refresh_tc2_body<128>(rplan, tm_q, tm_k, tm_v, tm_o, out, scores, (int)blockIdx.x, n_ref);
   else
@@ -828,8 +830,8 @@ cudaError_t launch_d(const Plan &plan, const void *q, const void *k, const void 
   if (e != cudaSuccess) return e;
   const int grid = plan.total_units < num_sms() ? plan.total_units : num_sms();
   if (grid <= 0) return cudaSuccess;
-  refresh_tc2_kernel<D><<<grid, THREADS, smem, st>>>(plan, tq, tk, tv, to, (__nv_bfloat16 *)out, scores);
-  return cudaGetLastError();
+  return launch_pdl(refresh_tc2_kernel<D>, dim3(grid), dim3(THREADS), smem, st, plan, tq, tk, tv, to,
+                    (__nv_bfloat16 *)out, scores);
 }
 
 }  // namespace
@@ -845,10 +847,9 @@ cudaError_t launch_mixed_tc(const Plan &rplan, const void *q, const void *k, con
   e = cudaFuncSetAttribute(mixed_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   if (grid <= 0) return cudaSuccess;
-  mixed_tc_kernel<<<grid, THREADS, smem, st>>>(rplan, tq, tk, tv, to, (__nv_bfloat16 *)out, scores, uplan,
-                                               (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k,
-                                               (const __nv_bfloat16 *)v, idx, (__nv_bfloat16 *)out_blk, n_ref);
-  return cudaGetLastError();
+  return launch_pdl(mixed_tc_kernel, dim3(grid), dim3(THREADS), smem, st, rplan, tq, tk, tv, to, (__nv_bfloat16 *)out,
+                    scores, uplan, (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k, (const __nv_bfloat16 *)v,
+                    idx, (__nv_bfloat16 *)out_blk, n_ref);
 }
 
 int num_sms_mixed() { return num_sms(); }

@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
 reuse_tc_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restrict__ q_blk,
                 const __nv_bfloat16 *__restrict__ k_cache, const __nv_bfloat16 *__restrict__ v_cache,
                 const int32_t *__restrict__ idx, __nv_bfloat16 *__restrict__ out) {
+  pdl_wait_then_trigger();
   reuse_tc_body(plan, q_blk, k_cache, v_cache, idx, out, (int)blockIdx.x, (int)gridDim.x);
 }
 
@@ -48,10 +49,9 @@ cudaError_t launch_reuse_tc(const Plan &plan, const void *q_blk, const void *k_c
   if (e != cudaSuccess) return e;
   const int grid = plan.total_units < num_sms_tc() ? plan.total_units : num_sms_tc();
   if (grid <= 0) return cudaSuccess;
-  reuse_tc_kernel<<<grid, kTThreads, kTBytes, st>>>(plan, (const __nv_bfloat16 *)q_blk,
-                                                    (const __nv_bfloat16 *)k_cache, (const __nv_bfloat16 *)v_cache,
-                                                    idx, (__nv_bfloat16 *)out);
-  return cudaGetLastError();
+  return launch_pdl(reuse_tc_kernel, dim3(grid), dim3(kTThreads), (size_t)kTBytes, st, plan,
+                    (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k_cache, (const __nv_bfloat16 *)v_cache, idx,
+                    (__nv_bfloat16 *)out);
 }
 
 }  // namespace dllm

@@ -71,6 +71,7 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
   __shared__ uint32_t s_prefix;
   __shared__ int s_krem;
 
+  pdl_wait_then_trigger();
   const int unit = blockIdx.x;
   const int b = plan_find(plan, unit);
   const ReqInfo &R = plan.r[b];
@@ -316,8 +317,7 @@ cudaError_t launch_select(const Plan &plan, const float *scores, int32_t *idx, c
   cudaError_t e = cudaFuncSetAttribute(select_heads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  select_heads_kernel<<<plan.total_units, kSelThreads, smem, st>>>(plan, scores, idx);
-  return cudaGetLastError();
+  return launch_pdl(select_heads_kernel, dim3(plan.total_units), dim3(kSelThreads), smem, st, plan, scores, idx);
 }
 
 cudaError_t launch_select_global(const Plan &plan, const float *scores, int32_t *idx, cudaStream_t st) {
