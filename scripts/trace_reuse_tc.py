@@ -45,10 +45,12 @@ for u in range(8):
     print(f"unit {u}: CTAs {m.sum()}, end median {np.median(rel(col[m])):.2f} us, "
           f"duration median {np.median((col[m] - prev[m]) / 1e3):.2f} us")
 c0 = tr[0, 0]
-print("CTA 0 chunks (us from CTA start): published, loader issued, S issued, softmax got S, bar.red done, "
-      "rescale done, P stored, P arrived, PV issued")
+print("CTA 0 stages (us from CTA start): published, loader issued")
 for t in range(min(24, int((ch[0] > 0).sum()))):
-    print(f"{t:3d} " + " ".join(f"{(ch[k, t] - c0) / 1e3:7.2f}" for k in (0, 1, 2, 3, 6, 7, 8, 4, 5)))
+    print(f"  st{t:3d} " + " ".join(f"{(ch[k, t] - c0) / 1e3:7.2f}" for k in (0, 1)))
+print("CTA 0 chunks: S issued, softmax got S, bar.red done, rescale done, P stored, P arrived, PV issued")
+for t in range(min(16, int((ch[2] > 0).sum()))):
+    print(f"  ch{t:3d} " + " ".join(f"{(ch[k, t] - c0) / 1e3:7.2f}" for k in (2, 3, 6, 7, 8, 4, 5)))
 print("unit: softmax row sums published, epilogue got O + sums, epilogue stores issued")
 for u in range(6):
     if ch[9, u] > 0:
