@@ -89,6 +89,13 @@ constexpr bool kNextDecode = DLLM_TC2_NEXTDECODE;  // decode the next unit mid-u
 // one barrier pair per K/V stage (K and V of a step land together, the stage is
 // released after the step's P.V): one wait and one commit fewer per step
 constexpr bool kKVMerged = DLLM_TC2_KVMERGED;
+#ifndef DLLM_TC2_POLY
+#define DLLM_TC2_POLY 0
+#endif
+// of every 8 exponential pairs of the softmax, this many run as a degree-3
+// polynomial on the FMA pipe instead of MUFU ex2 (16/clk/SM, the same rate at
+// which the tensor cores consume S elements at D = 128)
+constexpr int kPolyPairs = DLLM_TC2_POLY;
 
 template <int D>
 struct Cfg {
@@ -615,9 +622,15 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
 #pragma unroll
           for (int c = 0; c < 32; ++c) {
             const uint64_t x = ffma2(pack_f32x2(s[2 * c], s[2 * c + 1]), sl2x2, negm);
-            float x0, x1;
-            unpack_f32x2(x, x0, x1);
-            const float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
+            float p0, p1;
+            if ((c & 7) < kPolyPairs) {
+              unpack_f32x2(exp2_poly2(x), p0, p1);          // FMA pipe
+            } else {
+              float x0, x1;
+              unpack_f32x2(x, x0, x1);
+              p0 = fast_exp2(x0);                           // MUFU
+              p1 = fast_exp2(x1);
+            }
             acc[c & 3] = fadd2(acc[c & 3], pack_f32x2(p0, p1));
             pk[c] = pack_bf16(p0, p1);
           }
