@@ -255,6 +255,9 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph replay")
     ap.add_argument("--no-mixed", action="store_true",
                     help="C3: separate Refresh and Reuse launches instead of one mixed launch")
+    ap.add_argument("--fused-select", action="store_true",
+                    help="dllm_refresh_select_attn (select fused into the Refresh kernel when the library is built "
+                         "with DLLM_TC2_FUSEDSEL=1) instead of dllm_refresh_attn + dllm_select_heads")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -342,6 +345,9 @@ def main():
             bt = pt["batch"]
             pt["host"] = {"q": bt.q, "q_blk": bt.q_blk, "k_cache": bt.k_cache, "v_cache": bt.v_cache}
 
+    fused = args.fused_select   # dllm_refresh_select_attn (one call; fused only in a DLLM_TC2_FUSEDSEL=1 build)
+    fused_in_kernel = fused and "select_in_refresh=on" in lib.version()
+
     def step(ev=None):
         stream = torch.cuda.current_stream(dev)   # the capture stream while a graph is recorded
         if mixed:
@@ -350,11 +356,16 @@ def main():
             qb = pu["t"][1]
             if ev is not None:
                 ev[0].record(stream)
-            lib.mixed_attn(pr["p"], q, pr["buf"].out, pr["buf"].scores, pu["p"], qb, pu["buf"].idx, pu["buf"].out_blk,
-                           kc, vc, stream)
+            if fused:
+                lib.mixed_select_attn(pr["p"], q, pr["buf"].out, pr["buf"].scores, pr["buf"].idx, pu["p"], qb,
+                                      pu["buf"].idx, pu["buf"].out_blk, kc, vc, stream)
+            else:
+                lib.mixed_attn(pr["p"], q, pr["buf"].out, pr["buf"].scores, pu["p"], qb, pu["buf"].idx,
+                               pu["buf"].out_blk, kc, vc, stream)
             if ev is not None:
                 ev[1].record(stream)
-            lib.select_heads(pr["p"], pr["buf"].scores, pr["buf"].idx, stream)
+            if not fused:
+                lib.select_heads(pr["p"], pr["buf"].scores, pr["buf"].idx, stream)
             if ev is not None:
                 ev[2].record(stream)
                 ev[3].record(stream)
@@ -364,11 +375,14 @@ def main():
         for pt in parts_local:
             if pt["refresh"]:
                 q, qb, kc, vc = pt["t"]
-                lib.refresh_attn(pt["p"], q, kc, vc, pt["buf"].out, pt["buf"].scores, stream)
+                if fused:
+                    lib.refresh_select_attn(pt["p"], q, kc, vc, pt["buf"].out, pt["buf"].scores, pt["buf"].idx, stream)
+                else:
+                    lib.refresh_attn(pt["p"], q, kc, vc, pt["buf"].out, pt["buf"].scores, stream)
         if ev is not None:
             ev[1].record(stream)
         for pt in parts_local:
-            if pt["refresh"]:
+            if pt["refresh"] and not fused:
                 lib.select_heads(pt["p"], pt["buf"].scores, pt["buf"].idx, stream)
         if ev is not None:
             ev[2].record(stream)
@@ -470,7 +484,7 @@ def main():
         rows_all += rows
     a_ref = flops_refresh / statistics.mean(t_ref) / 1e12 if flops_refresh else 0.0
     a_reu = reuse_bytes / statistics.mean(t_reu) / 1e9 if reuse_bytes and not mixed else 0.0
-    a_sel = select_bytes / statistics.mean(t_sel) / 1e9 if select_bytes else 0.0
+    a_sel = select_bytes / statistics.mean(t_sel) / 1e9 if select_bytes and not fused else 0.0
     main_part = parts_local[0]
     buf = main_part["buf"]
     q, qb, kc, vc = main_part["t"]
@@ -570,7 +584,9 @@ def main():
                        "parallelism": f"request-sharded dp{world} (LPT), no data-path collective",
                        "l2": "flushed before every step (512 MiB write, outside the step events)",
                        "seed": synth.base_seed()},
-            "roofline": ({"bound": "tensor", "kernel": "dllm_refresh_attn (tcgen05)", "achieved": a_ref,
+            "roofline": ({"bound": "tensor", "kernel": ("dllm_refresh_select_attn (tcgen05 Refresh + select in one "
+                                                        "call: FLOP of Refresh only / time of both)") if fused else
+                          "dllm_refresh_attn (tcgen05)", "achieved": a_ref,
                           "peak": tf_peak, "unit": "TFLOP/s", "frac": a_ref / tf_peak, "traffic": traffic,
                           "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
                           "frac_of_sustained": (a_ref / tf_sust) if tf_sust else None} if not mixed else
@@ -585,12 +601,16 @@ def main():
                 "mixed": {"us": 1e6 * statistics.mean(t_ref), "refresh_flop": flops_refresh,
                           "reuse_bytes_unique": reuse_bytes, "reuse_bytes_logical": reuse_logical,
                           "roofline_us": 1e6 * (flops_refresh / (tf_peak * 1e12) + reuse_bytes / (hbm_peak * 1e9))},
-                "select": {"us": 1e6 * statistics.mean(t_sel), "GB/s": a_sel, "frac": a_sel / hbm_peak,
-                           "bytes_per_launch": select_bytes}} if mixed else {
+                "select": ({"in_one_call_with": "Refresh (timed with it)", "fused_in_kernel": fused_in_kernel,
+                            "bytes_per_launch": select_bytes}
+                           if fused else {"us": 1e6 * statistics.mean(t_sel), "GB/s": a_sel, "frac": a_sel / hbm_peak,
+                                          "bytes_per_launch": select_bytes})} if mixed else {
                 "refresh": {"us": 1e6 * statistics.mean(t_ref), "TFLOP/s": a_ref, "frac": a_ref / tf_peak,
                             "flop_per_launch": flops_refresh},
-                "select": {"us": 1e6 * statistics.mean(t_sel), "GB/s": a_sel, "frac": a_sel / hbm_peak,
-                           "bytes_per_launch": select_bytes},
+                "select": ({"in_one_call_with": "Refresh (timed with it)", "fused_in_kernel": fused_in_kernel,
+                            "bytes_per_launch": select_bytes}
+                           if fused else {"us": 1e6 * statistics.mean(t_sel), "GB/s": a_sel, "frac": a_sel / hbm_peak,
+                                          "bytes_per_launch": select_bytes}),
                 "reuse": {"us": 1e6 * statistics.mean(t_reu), "GB/s": a_reu, "frac": a_reu / hbm_peak,
                           "bytes_per_launch_unique": reuse_bytes, "bytes_per_launch_logical": reuse_logical,
                           "GB/s_logical": reuse_logical / statistics.mean(t_reu) / 1e9, "bound": "hbm",
@@ -601,7 +621,9 @@ def main():
             "launch_mode": launch_mode,
             "ms_per_step_eager": 1e3 * total_eager / args.steps,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": (2 if mixed else sum((2 * pt["refresh"] + pt["reuse"]) * ((pt["wl"].num_requests + 255) // 256)
+            "select_fused": fused_in_kernel,
+            "gpu_launches": ((1 if fused_in_kernel else 2) if mixed else
+                             sum(((1 if fused_in_kernel else 2) * pt["refresh"] + pt["reuse"]) * ((pt["wl"].num_requests + 255) // 256)
                                                  for pt in parts_local)) * args.steps,
             "clocks": clocks,
             "cpu_baseline": cpu,

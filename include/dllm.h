@@ -6,6 +6,8 @@
  *   dllm_refresh_attn       Refresh, Eq. 3 (§2.3) + the raw
  *                           per-head importance of Eq. 6 (§4.5)
  *   dllm_select_heads       local max-pool + per-head TopK (§4.5)
+ *   dllm_refresh_select_attn  the two above in one call (select fused into the
+ *                           Refresh kernel's epilogue when eligible)
  *   dllm_reuse_sparse_attn  Reuse, Eq. 4 (§2.3) over the
  *                           per-head key subsets of §4.5
  *
@@ -115,6 +117,20 @@ DLLM_API int dllm_refresh_attn(const dllm_problem *p, const void *q, const void 
  * Scores must be finite.  scores, idx: DEVICE. */
 DLLM_API int dllm_select_heads(const dllm_problem *p, const float *scores, int32_t *idx, void *stream);
 
+/* Refresh + selection in one call (next row N1, second half: the select fused
+ * into the Refresh epilogue; the paper selects at Refresh time
+ * §4.5).  Exactly dllm_refresh_attn(p, q, k_cache, v_cache, out, scores) followed
+ * by dllm_select_heads(p, scores, idx): out, scores and idx are bit-identical to
+ * the two calls.  In a library built with DLLM_TC2_FUSEDSEL=1, with D = 128 / 64
+ * and every n_ctx = L_b - blk_b <= 4096, the pool + TopK of each (b, h) runs
+ * inside the tcgen05 Refresh kernel (its epilogue warpgroup, right after the work
+ * unit that wrote that head's raw scores) and no select launch follows; the
+ * default build (measured faster) and every other case (or
+ * DLLM_FUSED_SELECT=0 in the environment) launch the two kernels.  scores and idx are required (not NULL); sizes from
+ * dllm_index_layout.  All tensors DEVICE. */
+DLLM_API int dllm_refresh_select_attn(const dllm_problem *p, const void *q, const void *k_cache,
+                                      const void *v_cache, void *out, float *scores, int32_t *idx, void *stream);
+
 /* Uniform selection, the Sparse-dLLM baseline (§2.4, Eq. 5):
  * S[c] = sum_h (pooled scores of head h)[c], summed in fp32 in ascending head
  * order; ONE top-k set per request (same pooling, tie rule and order as
@@ -162,6 +178,15 @@ DLLM_API int dllm_reuse_packed(const dllm_problem *p, const void *q_blk, const v
 DLLM_API int dllm_mixed_attn(const dllm_problem *p_refresh, const void *q, void *out, float *scores,
                              const dllm_problem *p_reuse, const void *q_blk, const int32_t *idx, void *out_blk,
                              const void *k_cache, const void *v_cache, void *stream);
+
+/* dllm_mixed_attn with the Refresh requests' selection fused in (as in
+ * dllm_refresh_select_attn): also writes idx_refresh = dllm_select_heads(
+ * p_refresh, scores, .) from inside the same launch when eligible, else by a
+ * select launch after it.  scores and idx_refresh required.  All DEVICE. */
+DLLM_API int dllm_mixed_select_attn(const dllm_problem *p_refresh, const void *q, void *out, float *scores,
+                                    int32_t *idx_refresh, const dllm_problem *p_reuse, const void *q_blk,
+                                    const int32_t *idx, void *out_blk, const void *k_cache, const void *v_cache,
+                                    void *stream);
 
 /* ---- Logit decomposition (next row N4; §4.3 "Logit
  * Decomposition", §5; SPEC.md:145-165 plan_logit_chunks /

@@ -35,7 +35,7 @@ cudaError_t launch_reuse_ws(const Plan &, const void *, const void *, const void
                             cudaStream_t);
 cudaError_t launch_mixed_tc(const Plan &rplan, const void *q, const void *k, const void *v, void *out, float *scores,
                             const Plan &uplan, const void *q_blk, const int32_t *idx, void *out_blk, int n_ref,
-                            int grid, cudaStream_t st);
+                            int grid, int32_t *sel_idx, cudaStream_t st);
 int num_sms_mixed();
 int64_t lmhead_vocab_tiles(int vocab);
 cudaError_t launch_lmhead_chunk(const void *hidden, const void *weight, int n_tok, int d_model, int vocab, int row0,
@@ -46,8 +46,9 @@ cudaError_t launch_reuse_tc(const Plan &, const void *, const void *, const void
 int refresh_mma_units(int L, int bs, int be, int H, bool with_scores);
 bool refresh_tc_supported(int D);
 int refresh_tc2_units(int L, int bs, int be, int H, bool with_scores);
-cudaError_t launch_refresh_tc2(const Plan &, const void *, const void *, const void *, void *, float *,
+cudaError_t launch_refresh_tc2(const Plan &, const void *, const void *, const void *, void *, float *, int32_t *,
                                cudaStream_t);
+int fused_select_max_n();
 int refresh_tc_units(int L, int bs, int be, int H, bool with_scores);
 cudaError_t launch_refresh_tc(const Plan &, const void *, const void *, const void *, void *, float *,
                               cudaStream_t);
@@ -245,8 +246,13 @@ int dllm_index_layout(const dllm_problem *p, int32_t *k_out, int64_t *total_idx,
   return ok();
 }
 
-int dllm_refresh_attn(const dllm_problem *p, const void *q, const void *k_cache, const void *v_cache, void *out,
-                      float *scores, void *stream) {
+}  // extern "C"
+
+namespace {
+// Refresh (+ optionally the fused select): sel_idx != NULL asks the tcgen05 kernel
+// to run pool + TopK in its epilogue warpgroup (caller checked fused_ok()).
+int refresh_impl(const dllm_problem *p, const void *q, const void *k_cache, const void *v_cache, void *out,
+                 float *scores, int32_t *sel_idx, void *stream) {
   Layout lay;
   int st = make_layout(p, lay);
   if (st) return st;
@@ -269,12 +275,47 @@ int dllm_refresh_attn(const dllm_problem *p, const void *q, const void *k_cache,
                          : refresh_mma_units(L, bs, be, H, with_scores);
     });
     pl.with_scores = with_scores;
-    cudaError_t e = impl == 2 ? launch_refresh_tc2(pl, q, k_cache, v_cache, out, scores, s)
+    cudaError_t e = impl == 2 ? launch_refresh_tc2(pl, q, k_cache, v_cache, out, scores, sel_idx, s)
                     : impl == 1 ? launch_refresh_tc(pl, q, k_cache, v_cache, out, scores, s)
                                 : launch_refresh_mma(pl, q, k_cache, v_cache, out, scores, s);
     if (e != cudaSuccess) return cuda_fail(e, "refresh launch");
   }
   return ok();
+}
+
+// the select can run inside the Refresh kernel: tcgen05 path, every candidate set
+// small enough for the epilogue warpgroup's registers
+bool fused_ok(const dllm_problem *p, const float *scores, const int32_t *idx) {
+  if (!scores || !idx || !refresh_tc_supported(p->head_dim) || refresh_impl_env() != 2) return false;
+  if (const char *e = getenv("DLLM_FUSED_SELECT"))
+    if (e[0] == '0') return false;
+  for (int b = 0; b < p->num_requests; ++b)
+    if (p->seq_len[b] - (p->blk_end[b] - p->blk_start[b]) > fused_select_max_n()) return false;
+  return true;
+}
+}  // namespace
+
+extern "C" {
+
+int dllm_refresh_attn(const dllm_problem *p, const void *q, const void *k_cache, const void *v_cache, void *out,
+                      float *scores, void *stream) {
+  return refresh_impl(p, q, k_cache, v_cache, out, scores, nullptr, stream);
+}
+
+int dllm_refresh_select_attn(const dllm_problem *p, const void *q, const void *k_cache, const void *v_cache,
+                             void *out, float *scores, int32_t *idx, void *stream) {
+  Layout lay;
+  int st = make_layout(p, lay);
+  if (st) return st;
+  if (p->num_requests == 0) return ok();
+  if (!scores || !idx) return fail(DLLM_ERR_INVALID_ARG, "refresh_select: NULL scores / idx");
+  for (int b = 0; b < p->num_requests; ++b)
+    if (p->seq_len[b] > DLLM_MAX_SELECT_LEN)
+      return fail(DLLM_ERR_UNSUPPORTED, "select: request %d seq_len=%d > %d", b, p->seq_len[b], DLLM_MAX_SELECT_LEN);
+  if (fused_ok(p, scores, idx)) return refresh_impl(p, q, k_cache, v_cache, out, scores, idx, stream);
+  st = refresh_impl(p, q, k_cache, v_cache, out, scores, nullptr, stream);
+  if (st) return st;
+  return dllm_select_heads(p, scores, idx, stream);
 }
 
 int dllm_select_heads(const dllm_problem *p, const float *scores, int32_t *idx, void *stream) {
@@ -415,9 +456,12 @@ int dllm_check_indices(const dllm_problem *p, const int32_t *idx, int32_t *d_vio
   return ok();
 }
 
-int dllm_mixed_attn(const dllm_problem *p_refresh, const void *q, void *out, float *scores,
-                    const dllm_problem *p_reuse, const void *q_blk, const int32_t *idx, void *out_blk,
-                    const void *k_cache, const void *v_cache, void *stream) {
+}  // extern "C"
+
+namespace {
+int mixed_impl(const dllm_problem *p_refresh, const void *q, void *out, float *scores, int32_t *sel_idx,
+               const dllm_problem *p_reuse, const void *q_blk, const int32_t *idx, void *out_blk,
+               const void *k_cache, const void *v_cache, void *stream) {
   if (!p_refresh || !p_reuse) return fail(DLLM_ERR_INVALID_ARG, "mixed: NULL problem");
   Layout lr, lu;
   int st = make_layout(p_refresh, lr);
@@ -435,7 +479,8 @@ int dllm_mixed_attn(const dllm_problem *p_refresh, const void *q, void *out, flo
     // not expressible as one launch (a phase is empty, > kMaxReqPerLaunch requests, or
     // a head dim / A-B override outside the two tcgen05 kernels): the same work as
     // separate launches, same results
-    st = dllm_refresh_attn(p_refresh, q, k_cache, v_cache, out, scores, stream);
+    st = sel_idx ? dllm_refresh_select_attn(p_refresh, q, k_cache, v_cache, out, scores, sel_idx, stream)
+                 : dllm_refresh_attn(p_refresh, q, k_cache, v_cache, out, scores, stream);
     if (st) return st;
     return dllm_reuse_sparse_attn(p_reuse, q_blk, k_cache, v_cache, idx, out_blk, stream);
   }
@@ -470,9 +515,34 @@ int dllm_mixed_attn(const dllm_problem *p_refresh, const void *q, void *out, flo
   int n_reu = nsm - n_ref;
   if (n_reu > up.total_units) n_reu = up.total_units;
   cudaError_t e = launch_mixed_tc(rp, q, k_cache, v_cache, out, scores, up, q_blk, idx, out_blk, n_ref, n_ref + n_reu,
-                                  (cudaStream_t)stream);
+                                  sel_idx, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "mixed launch");
   return ok();
+}
+}  // namespace
+
+extern "C" {
+
+int dllm_mixed_attn(const dllm_problem *p_refresh, const void *q, void *out, float *scores,
+                    const dllm_problem *p_reuse, const void *q_blk, const int32_t *idx, void *out_blk,
+                    const void *k_cache, const void *v_cache, void *stream) {
+  return mixed_impl(p_refresh, q, out, scores, nullptr, p_reuse, q_blk, idx, out_blk, k_cache, v_cache, stream);
+}
+
+int dllm_mixed_select_attn(const dllm_problem *p_refresh, const void *q, void *out, float *scores, int32_t *idx_refresh,
+                           const dllm_problem *p_reuse, const void *q_blk, const int32_t *idx, void *out_blk,
+                           const void *k_cache, const void *v_cache, void *stream) {
+  if (!p_refresh) return fail(DLLM_ERR_INVALID_ARG, "mixed: NULL problem");
+  if (!scores || !idx_refresh) return fail(DLLM_ERR_INVALID_ARG, "mixed_select: NULL scores / idx_refresh");
+  for (int b = 0; b < p_refresh->num_requests; ++b)
+    if (p_refresh->seq_len[b] > DLLM_MAX_SELECT_LEN)
+      return fail(DLLM_ERR_UNSUPPORTED, "select: request %d seq_len=%d > %d", b, p_refresh->seq_len[b],
+                  DLLM_MAX_SELECT_LEN);
+  if (fused_ok(p_refresh, scores, idx_refresh))
+    return mixed_impl(p_refresh, q, out, scores, idx_refresh, p_reuse, q_blk, idx, out_blk, k_cache, v_cache, stream);
+  int st = mixed_impl(p_refresh, q, out, scores, nullptr, p_reuse, q_blk, idx, out_blk, k_cache, v_cache, stream);
+  if (st) return st;
+  return dllm_select_heads(p_refresh, scores, idx_refresh, stream);
 }
 
 int dllm_logit_chunks(int64_t n_logit, int32_t max_num_logits, int32_t *chunk_sizes, int32_t capacity) {
@@ -539,9 +609,11 @@ const char *dllm_status_string(int status) {
 const char *dllm_last_error(void) { return g_last_error.c_str(); }
 
 const char *dllm_version(void) {
-  return "libdllm sm_100a: refresh=tcgen05/TMEM+TMA (mma.sync for D<64), select=radix-topk, "
-         "reuse=paged cp.async gather + tcgen05 (D=128; mma.sync otherwise), mixed=one-launch Refresh+Reuse, "
-         "lm_head=tcgen05 GEMM + fused argmax";
+  static const std::string v = std::string(
+      "libdllm sm_100a: refresh=tcgen05/TMEM+TMA (mma.sync for D<64), select=radix-topk, "
+      "reuse=paged cp.async gather + tcgen05 (D=128; mma.sync otherwise), mixed=one-launch Refresh+Reuse, "
+      "lm_head=tcgen05 GEMM + fused argmax, select_in_refresh=") + (fused_select_max_n() > 0 ? "on" : "off");
+  return v.c_str();
 }
 
 }  // extern "C"

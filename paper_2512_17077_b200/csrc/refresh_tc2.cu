@@ -39,7 +39,7 @@
 #include "reuse_tc_body.cuh"
 
 #ifdef DLLM_TRACE
-__device__ long long g_trace2[28][512];
+__device__ long long g_trace2[34][512];
 #define TRACE2(kind, it)                                                   \
   do {                                                                     \
     if (blockIdx.x == 0 && (it) < 512) g_trace2[kind][it] = clock64();     \
@@ -90,12 +90,19 @@ constexpr bool kNextDecode = DLLM_TC2_NEXTDECODE;  // decode the next unit mid-u
 // released after the step's P.V): one wait and one commit fewer per step
 constexpr bool kKVMerged = DLLM_TC2_KVMERGED;
 #ifndef DLLM_TC2_POLY
-#define DLLM_TC2_POLY 0
+#define DLLM_TC2_POLY 2   // 2 of 8 (A/B: 0 -> 2 is +2% at C1, +1% at C2; 3 is slower)
 #endif
 // of every 8 exponential pairs of the softmax, this many run as a degree-3
 // polynomial on the FMA pipe instead of MUFU ex2 (16/clk/SM, the same rate at
 // which the tensor cores consume S elements at D = 128)
 constexpr int kPolyPairs = DLLM_TC2_POLY;
+#ifndef DLLM_TC2_FUSEDSEL
+// 1: pool + TopK fused into the epilogue warpgroup (dllm_refresh_select_attn).  Off by
+// default: measured ~13 us per (b, h) selection at C1 (~25k clk, issue-starved beside
+// the softmax warps, and its unrolled code bloats the kernel ~2x), which made the
+// fused call 16% slower than Refresh + the select launch at C1 (1% faster at C2).
+#define DLLM_TC2_FUSEDSEL 0
+#endif
 
 template <int D>
 struct Cfg {
@@ -143,6 +150,8 @@ struct Unit {
   int origin0, origin1;
   int wend0, wend1;
   int sc0, sc1;   // importance epilogue on tile 0 / 1
+  int k;          // k_b (fused select)
+  int64_t idx_off;
 };
 
 // a / b and a % b for 0 <= a < 2^24, 1 <= b < 2^24: fp32 quotient (off by at most
@@ -174,6 +183,7 @@ __device__ __forceinline__ void decode_unit(const Plan &pl, const ReqInfo *rs, i
   const ReqInfo &R = rs[lo];
   u.L = R.L; u.bs = R.bs; u.be = R.be;
   u.q_off = R.q_off; u.bt_row = R.bt_row; u.score_off = R.score_off;
+  u.k = R.k; u.idx_off = R.idx_off;
   const int nreg = regular_tiles(u.L);
   const bool extra = pl.with_scores && straddles(u.bs, u.be);
   const int ntiles = nreg + (extra ? 1 : 0);
@@ -206,6 +216,157 @@ __device__ __forceinline__ void decode_unit(const Plan &pl, const ReqInfo *rs, i
   u.sc1 = pl.with_scores && u.tile1 && (t1 == nreg || (!extra && t1 == u.bs / TBM));
 }
 
+// ---------------------------------------------------------------- fused select
+// Pool + per-head TopK (Eq. 6 + TopK, §4.5) of ONE (request,
+// head) by the 128 epilogue-warpgroup threads, right after the unit whose softmax
+// warps wrote that head's raw scores (select fused into the
+// Refresh epilogue).  The same definition and the same integer decisions as
+// select_heads_kernel (select.cu; R2-R9): candidates C = [0,bs) ++
+// [be,L), window of half-width w/2 clipped to the compacted axis, order-preserving
+// 32-bit keys (-0 == +0), an exact 4-pass 8-bit MSB radix select of the k-th key,
+// every key above it plus the lowest-index keys equal to it, written as ascending
+// sequence positions.  Thread t owns the contiguous candidates [t P, t P + P),
+// P = ceil(n/128) <= kFSelPer, held in registers, so the ascending output slots
+// come from one block scan of per-thread counts.
+constexpr int kFSelThreads = 128;
+constexpr int kFSelPer = 32;                            // n_ctx <= 4096 (host-checked)
+constexpr int kFSelMaxN = kFSelThreads * kFSelPer;
+constexpr int kFSelBar = 5;                             // named barrier of the epilogue warpgroup
+constexpr int kFSelHalfMax = 4;                         // windows w <= 9 pool from registers
+
+__device__ __forceinline__ uint32_t fsel_key(float f) {
+  const uint32_t u = __float_as_uint(f);
+  if ((u & 0x7fffffffu) == 0u) return 0x80000000u;       // +-0 -> one key
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// raw: the head's L raw scores (written by this CTA in this kernel: plain loads,
+// not the read-only path); scratch: >= 256 + 8 + 2 words of shared memory
+__device__ __forceinline__ void fused_select(const float *raw, const int L, const int bs, const int be, const int half,
+                                          const int k, int32_t *__restrict__ out, int *scratch, const int t) {
+  int *hist = scratch;                                   // [256]
+  int *wbuf = scratch + 256;                             // [4]
+  int *sh = scratch + 264;                               // [2]: prefix, krem
+  const int blk = be - bs, n = L - blk;
+  const int P = (n + kFSelThreads - 1) / kFSelThreads;
+  const int c0 = t * P;
+  const int nv = max(0, min(P, n - c0));
+  uint32_t key[kFSelPer];
+  if (half <= kFSelHalfMax) {
+    // the thread's P candidates and the half-windows around them: all loads in
+    // flight together (one L2 round trip), -inf outside [0, n) == clipping
+    float rv[kFSelPer + 2 * kFSelHalfMax];
+#pragma unroll
+    for (int i = 0; i < kFSelPer + 2 * kFSelHalfMax; ++i) {
+      const int c = c0 - half + i;
+      rv[i] = (i < P + 2 * half && c >= 0 && c < n) ? raw[c < bs ? c : c + blk] : -INFINITY;
+    }
+#pragma unroll
+    for (int i = 0; i < kFSelPer; ++i) {
+      float m = rv[i];
+#pragma unroll
+      for (int d = 1; d <= 2 * kFSelHalfMax; ++d)
+        if (d <= 2 * half) m = fmaxf(m, rv[i + d]);
+      key[i] = i < nv ? fsel_key(m) : 0u;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kFSelPer; ++i) {
+      uint32_t kk = 0u;
+      if (i < nv) {
+        const int c = c0 + i;
+        const int lo = max(0, c - half), hi = min(n - 1, c + half);
+        float m = -INFINITY;
+        for (int j = lo; j <= hi; ++j) m = fmaxf(m, raw[j < bs ? j : j + blk]);
+        kk = fsel_key(m);
+      }
+      key[i] = kk;
+    }
+  }
+  uint32_t prefix = 0u, mask = 0u;
+  int krem = k;
+#pragma unroll 1
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = t; i < 256; i += kFSelThreads) hist[i] = 0;
+    ptx::named_bar_sync(kFSelBar, kFSelThreads);
+    // warp-aggregated: the keys crowd a few bins (similar exponents), so lanes with
+    // equal bins are merged (match.any) into one shared atomic; P is CTA-uniform
+#pragma unroll
+    for (int i = 0; i < kFSelPer; ++i) {
+      if (i >= P) break;
+      const bool act = i < nv && (key[i] & mask) == prefix;
+      const uint32_t bin = act ? ((key[i] >> shift) & 0xffu) : 0x100u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+      if (act && (t & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
+    }
+    ptx::named_bar_sync(kFSelBar, kFSelThreads);
+    if (t < 32) {
+      // lane l owns bins [8 (31 - l), 8 (31 - l) + 8): lane 0 the top bins
+      const int base = 8 * (31 - t);
+      int cnt[8], sum = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { cnt[i] = hist[base + 7 - i]; sum += cnt[i]; }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (t >= o) incl += y;
+      }
+      const int above = incl - sum;
+      if (above < krem && krem <= incl) {
+        int acc = above;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (acc + cnt[i] >= krem) {
+            sh[0] = (int)(prefix | ((uint32_t)(base + 7 - i) << shift));
+            sh[1] = krem - acc;
+            break;
+          }
+          acc += cnt[i];
+        }
+      }
+    }
+    ptx::named_bar_sync(kFSelBar, kFSelThreads);
+    prefix = (uint32_t)sh[0];
+    krem = sh[1];
+    mask |= 0xffu << shift;
+  }
+  // compaction: slot of a selected candidate = #above before it + min(#equal before it, krem)
+  int gt = 0, eq = 0;
+#pragma unroll
+  for (int i = 0; i < kFSelPer; ++i)
+    if (i < nv) { gt += key[i] > prefix; eq += key[i] == prefix; }
+  const int v = gt | (eq << 16);
+  const int lane = t & 31, w = t >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wbuf[w] = x;
+  ptx::named_bar_sync(kFSelBar, kFSelThreads);
+  int basew = 0;
+  for (int i = 0; i < w; ++i) basew += wbuf[i];
+  const int pre = basew + x - v;
+  int gt_pre = pre & 0xffff, eq_pre = pre >> 16;
+#pragma unroll
+  for (int i = 0; i < kFSelPer; ++i) {
+    if (i < nv) {
+      const int c = c0 + i;
+      const int pos = c < bs ? c : c + blk;
+      if (key[i] > prefix) {
+        out[gt_pre + min(eq_pre, krem)] = pos;
+        ++gt_pre;
+      } else if (key[i] == prefix) {
+        if (eq_pre < krem) out[gt_pre + eq_pre] = pos;
+        ++eq_pre;
+      }
+    }
+  }
+  ptx::named_bar_sync(kFSelBar, kFSelThreads);        // scratch free again
+}
+
 // The kernel body, shared by refresh_tc2_kernel and the single-launch mixed
 // Refresh/Reuse kernel below: CTA `cta` of `ncta` CTAs working on this plan.  The
 // tensor maps are references to __grid_constant__ kernel parameters.
@@ -213,7 +374,7 @@ template <int D>
 __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
                                                  const CUtensorMap &tm_v, const CUtensorMap &tm_o,
                                                  __nv_bfloat16 *__restrict__ out, float *__restrict__ scores,
-                                                 const int cta, const int ncta) {
+                                                 int32_t *__restrict__ sel_idx, const int cta, const int ncta) {
   using C = Cfg<D>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
@@ -534,6 +695,7 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
         DLLM_TMEM_LD32(tS + 0, (sr + 0));
         DLLM_TMEM_LD32(tS + 32, (sr + 32));
         ptx::tmem_wait_ld();
+        if (threadIdx.x == 0) TRACE2(28, sc);
         float *s = reinterpret_cast<float *>(sr);
         if (sc_on) {
           // importance: column max of the UNSCALED S over the block rows
@@ -588,6 +750,7 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
           for (int i = 0; i < 8; ++i) t[i] = fmaxf(t[i], s[56 + i]);
           mx = fmax3(fmax3(t[0], t[1], t[2]), fmax3(t[3], t[4], t[5]), fmaxf(t[6], t[7])) * sl2;
         }
+        if (threadIdx.x == 0) TRACE2(29, sc);
         if (j == 0) {
           m_used = mx;
         } else {
@@ -634,6 +797,7 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
             acc[c & 3] = fadd2(acc[c & 3], pack_f32x2(p0, p1));
             pk[c] = pack_bf16(p0, p1);
           }
+          if (threadIdx.x == 0) TRACE2(30, sc);
           DLLM_TMEM_ST32(tS, pk);
           float a0, a1, a2, a3;
           unpack_f32x2(fadd2(acc[0], acc[1]), a0, a1);
@@ -641,6 +805,7 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
           lsum += (a0 + a1) + (a2 + a3);
         }
         ptx::tmem_wait_st();
+        if (threadIdx.x == 0) TRACE2(31, sc);
         ptx::tc_fence_before();
         __syncwarp();
         if ((threadIdx.x & 127) == 0) TRACE2(4 + wg, sc);
@@ -666,6 +831,8 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
     uint8_t *stg = gb + C::kOffStage + wq * 32 * 64;
     const uint32_t stg_s = sb + C::kOffStage + wq * 32 * 64;
     int oc[2] = {0, 0};
+    int selc = 0;
+    (void)selc;
     for (int unit = cta; unit < plan.total_units; unit += ncta) {
       Unit u;
       decode_unit(plan, rs, unit, u, dcur);
@@ -716,6 +883,18 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
           }
         }
       }
+      if (DLLM_TC2_FUSEDSEL && sel_idx != nullptr && scores != nullptr && (u.sc0 || u.sc1) && u.k > 0) {
+        // this unit's softmax warps wrote the head's raw scores (every key, all steps)
+        // before their row-sum arrivals, which the O loop above acquired
+        if (lane == 0) ptx::bulk_wait_group_read0();   // staging tile becomes select scratch
+        ptx::named_bar_sync(kFSelBar, kFSelThreads);
+        if (warp == kEpi0 && lane == 0) TRACE2(32, selc);
+        fused_select(scores + u.score_off + (int64_t)u.h * u.L, u.L, u.bs, u.be, plan.window >> 1, u.k,
+                     sel_idx + u.idx_off + (int64_t)u.h * u.k, reinterpret_cast<int *>(gb + C::kOffStage),
+                     (warp - kEpi0) * 32 + lane);
+        if (warp == kEpi0 && lane == 0) TRACE2(33, selc);
+        ++selc;
+      }
     }
     if (lane == 0) ptx::bulk_wait_group0();
   } else {
@@ -741,9 +920,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CUtensorMap tm_q,
                    const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                    const __grid_constant__ CUtensorMap tm_o, __nv_bfloat16 *__restrict__ out,
-                   float *__restrict__ scores) {
+                   float *__restrict__ scores, int32_t *__restrict__ sel_idx) {
   pdl_wait_then_trigger();
-  refresh_tc2_body<D>(plan, tm_q, tm_k, tm_v, tm_o, out, scores, (int)blockIdx.x, (int)gridDim.x);
+  refresh_tc2_body<D>(plan, tm_q, tm_k, tm_v, tm_o, out, scores, sel_idx, (int)blockIdx.x, (int)gridDim.x);
 }
 
 // Single-launch mixed-phase batch (the paper's single varlen
@@ -760,10 +939,11 @@ mixed_tc_kernel(const __grid_constant__ Plan rplan, const __grid_constant__ CUte
                 const __grid_constant__ CUtensorMap tm_o, __nv_bfloat16 *__restrict__ out, float *__restrict__ scores,
                 const __grid_constant__ Plan uplan, const __nv_bfloat16 *__restrict__ q_blk,
                 const __nv_bfloat16 *__restrict__ k_cache, const __nv_bfloat16 *__restrict__ v_cache,
-                const int32_t *__restrict__ idx, __nv_bfloat16 *__restrict__ out_blk, const int n_ref) {
+                const int32_t *__restrict__ idx, __nv_bfloat16 *__restrict__ out_blk, const int n_ref,
+                int32_t *__restrict__ sel_idx) {
   pdl_wait_then_trigger();
   if ((int)blockIdx.x < n_ref)
-    refresh_tc2_body<128>(rplan, tm_q, tm_k, tm_v, tm_o, out, scores, (int)blockIdx.x, n_ref);
+    refresh_tc2_body<128>(rplan, tm_q, tm_k, tm_v, tm_o, out, scores, sel_idx, (int)blockIdx.x, n_ref);
   else
     rtc::reuse_tc_body(uplan, q_blk, k_cache, v_cache, idx, out_blk, (int)blockIdx.x - n_ref,
                        (int)gridDim.x - n_ref);
@@ -834,7 +1014,7 @@ cudaError_t make_maps(const Plan &plan, const void *q, const void *k, const void
 
 template <int D>
 cudaError_t launch_d(const Plan &plan, const void *q, const void *k, const void *v, void *out, float *scores,
-                     cudaStream_t st) {
+                     int32_t *sel_idx, cudaStream_t st) {
   CUtensorMap tq, tk, tv, to;
   cudaError_t me = make_maps<D>(plan, q, k, v, out, tq, tk, tv, to);
   if (me != cudaSuccess) return me;
@@ -844,14 +1024,14 @@ cudaError_t launch_d(const Plan &plan, const void *q, const void *k, const void 
   const int grid = plan.total_units < num_sms() ? plan.total_units : num_sms();
   if (grid <= 0) return cudaSuccess;
   return launch_pdl(refresh_tc2_kernel<D>, dim3(grid), dim3(THREADS), smem, st, plan, tq, tk, tv, to,
-                    (__nv_bfloat16 *)out, scores);
+                    (__nv_bfloat16 *)out, scores, sel_idx);
 }
 
 }  // namespace
 
 cudaError_t launch_mixed_tc(const Plan &rplan, const void *q, const void *k, const void *v, void *out, float *scores,
                             const Plan &uplan, const void *q_blk, const int32_t *idx, void *out_blk, int n_ref,
-                            int grid, cudaStream_t st) {
+                            int grid, int32_t *sel_idx, cudaStream_t st) {
   if (rplan.D != 128 || uplan.D != 128) return cudaErrorInvalidValue;
   CUtensorMap tq, tk, tv, to;
   cudaError_t e = make_maps<128>(rplan, q, k, v, out, tq, tk, tv, to);
@@ -862,10 +1042,12 @@ cudaError_t launch_mixed_tc(const Plan &rplan, const void *q, const void *k, con
   if (grid <= 0) return cudaSuccess;
   return launch_pdl(mixed_tc_kernel, dim3(grid), dim3(THREADS), smem, st, rplan, tq, tk, tv, to, (__nv_bfloat16 *)out,
                     scores, uplan, (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k, (const __nv_bfloat16 *)v,
-                    idx, (__nv_bfloat16 *)out_blk, n_ref);
+                    idx, (__nv_bfloat16 *)out_blk, n_ref, sel_idx);
 }
 
 int num_sms_mixed() { return num_sms(); }
+
+int fused_select_max_n() { return DLLM_TC2_FUSEDSEL ? kFSelMaxN : 0; }
 
 int refresh_tc2_units(int L, int bs, int be, int H, bool with_scores) {
   const int nt = regular_tiles(L) + ((with_scores && straddles(bs, be)) ? 1 : 0);
@@ -873,10 +1055,10 @@ int refresh_tc2_units(int L, int bs, int be, int H, bool with_scores) {
 }
 
 cudaError_t launch_refresh_tc2(const Plan &plan, const void *q, const void *k, const void *v, void *out,
-                               float *scores, cudaStream_t st) {
+                               float *scores, int32_t *sel_idx, cudaStream_t st) {
   switch (plan.D) {
-    case 64: return launch_d<64>(plan, q, k, v, out, scores, st);
-    case 128: return launch_d<128>(plan, q, k, v, out, scores, st);
+    case 64: return launch_d<64>(plan, q, k, v, out, scores, sel_idx, st);
+    case 128: return launch_d<128>(plan, q, k, v, out, scores, sel_idx, st);
   }
   return cudaErrorInvalidValue;
 }

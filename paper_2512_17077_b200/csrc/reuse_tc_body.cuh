@@ -61,8 +61,17 @@ constexpr int kTChunk = 128;        // keys per ring stage (MMA M of S^T)
 #ifndef DLLM_RTC_SLEEP_MMA
 #define DLLM_RTC_SLEEP_MMA 0
 #endif
+#ifndef DLLM_RTC_PVEARLY
+#define DLLM_RTC_PVEARLY 1   // MMA warp polls: P.V(t-1) is issued before S(t) when chunk t is not loaded yet
+#endif
+#ifndef DLLM_RTC_PREFETCH
+#define DLLM_RTC_PREFETCH 1  // translator: 0 = every index list / block-table row of the CTA prefetched to L2 up
+                             // front (lane-parallel), 1 = the next unit's, prefetched when a unit starts
+#endif
 
 constexpr int kTNS = DLLM_RTC_NS;
+constexpr bool kPvEarly = DLLM_RTC_PVEARLY != 0;
+constexpr bool kRollingPrefetch = DLLM_RTC_PREFETCH == 1;
 constexpr int kTNT = 4;             // translation ring depth (chunks)
 constexpr int kTTG = 4;             // chunks translated per batch
 // Warp roles (16 warps; the warp schedulers favour the highest warp id among the
@@ -263,7 +272,8 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
   if (warp == kTransWarp) {
     // ============================ translator (+ Q rows) ============================
     // every index list and block-table row this CTA will translate, pulled into L2
-    for (int unit = cta + lane * ncta; unit < plan.total_units; unit += 32 * ncta) {
+    // (lane-parallel: divergent plan lookups, queued ahead of the first unit's loads)
+    for (int unit = cta + lane * ncta; !kRollingPrefetch && unit < plan.total_units; unit += 32 * ncta) {
       TUnit u;
       tdecode(plan, unit, u);
       if (u.k > 0) {
@@ -283,6 +293,24 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
     for (int unit = cta; unit < plan.total_units; unit += ncta) {
       TUnit u;
       tdecode(plan, unit, u);
+      if (kRollingPrefetch && unit + ncta < plan.total_units) {
+        // the next unit's index list and block-table row go to L2 while this one is
+        // translated (warp-uniform lookup, one bulk prefetch each)
+        TUnit v;
+        tdecode(plan, unit + ncta, v);
+        if (lane == 0 && v.k > 0) {
+          const uintptr_t a0 = reinterpret_cast<uintptr_t>(idx + v.idx_off) & ~uintptr_t(15);
+          const uintptr_t a1 = (reinterpret_cast<uintptr_t>(idx + v.idx_off + v.k) + 15) & ~uintptr_t(15);
+          ptx::bulk_prefetch_l2(reinterpret_cast<const void *>(a0), (uint32_t)(a1 - a0));
+        }
+        if (lane == 1 && v.bt_row != u.bt_row) {
+          const uintptr_t b0 = reinterpret_cast<uintptr_t>(plan.block_table + (int64_t)v.bt_row * plan.pages_per_req) &
+                               ~uintptr_t(15);
+          const uintptr_t b1 = (reinterpret_cast<uintptr_t>(plan.block_table + (int64_t)(v.bt_row + 1) * plan.pages_per_req) +
+                                15) & ~uintptr_t(15);
+          ptx::bulk_prefetch_l2(reinterpret_cast<const void *>(b0), (uint32_t)(b1 - b0));
+        }
+      }
       const int32_t *my_idx = idx + u.idx_off;
       const int32_t *bt = plan.block_table + (int64_t)u.bt_row * plan.pages_per_req;
       const int nchunks = (u.nk + kTChunk - 1) / kTChunk;
@@ -420,6 +448,18 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
       wait_bo<DLLM_RTC_SLEEP_MMA>(b_qfull + 8 * qb, (uc >> 1) & 1);
       for (int c = 0; c < nchunks; ++c, ++t) {
         const int s = t % NS, sbuf = t & 1;
+        if (kPvEarly) {
+          // P.V(t-1) goes out as soon as its P is ready, even when chunk t's K/V
+          // rows are still in flight: its stage is released that much earlier
+          while (!(ptx::mbar_test_wait(b_kvfull + 8 * s, (t / NS) & 1) &&
+                   ptx::mbar_test_wait(b_sfree + 8 * sbuf, ((t >> 1) & 1) ^ 1))) {
+            if (pv_t >= 0 && ptx::mbar_test_wait(b_pfull + 8 * (pv_t & 1), (pv_t >> 1) & 1) &&
+                (!pv_first || ptx::mbar_test_wait(b_ofree + 8 * pv_ob, ((pv_uc >> 1) & 1) ^ 1))) {
+              issue_pv();
+              pv_t = -1;
+            }
+          }
+        }
         wait_bo<DLLM_RTC_SLEEP_MMA>(b_kvfull + 8 * s, (t / NS) & 1);
         wait_bo<DLLM_RTC_SLEEP_MMA>(b_sfree + 8 * sbuf, ((t >> 1) & 1) ^ 1);
         ptx::fence_proxy_async_smem();   // cp.async (generic proxy) data -> tensor core (async proxy)
@@ -441,7 +481,7 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
       }
       // the unit's last P.V goes out now, not behind the next unit's first K chunk:
       // the epilogue waits for it
-      issue_pv();
+      if (pv_t >= 0) issue_pv();
       pv_t = -1;
     }
   } else if (warp < kEpi0) {

@@ -27,6 +27,7 @@ DLLM_ERR_K_RANGE = -4
 DLLM_ERR_CUDA = -5
 
 EXPORTED = ("dllm_keep_count", "dllm_index_layout", "dllm_refresh_attn", "dllm_select_heads", "dllm_select_global",
+            "dllm_refresh_select_attn", "dllm_mixed_select_attn",
             "dllm_reuse_sparse_attn", "dllm_pack_kv", "dllm_reuse_packed", "dllm_mixed_attn", "dllm_logit_chunks",
             "dllm_lm_head_workspace_bytes", "dllm_lm_head_argmax", "dllm_check_indices", "dllm_status_string",
             "dllm_last_error", "dllm_version")
@@ -82,6 +83,10 @@ def _load() -> ctypes.CDLL:
     lib.dllm_reuse_packed.restype = ctypes.c_int
     lib.dllm_mixed_attn.argtypes = [P, vp, vp, vp, P, vp, vp, vp, vp, vp, vp]
     lib.dllm_mixed_attn.restype = ctypes.c_int
+    lib.dllm_refresh_select_attn.argtypes = [P, vp, vp, vp, vp, vp, vp, vp]
+    lib.dllm_refresh_select_attn.restype = ctypes.c_int
+    lib.dllm_mixed_select_attn.argtypes = [P, vp, vp, vp, vp, P, vp, vp, vp, vp, vp, vp]
+    lib.dllm_mixed_select_attn.restype = ctypes.c_int
     lib.dllm_logit_chunks.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.c_int32]
     lib.dllm_logit_chunks.restype = ctypes.c_int
     lib.dllm_lm_head_workspace_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
@@ -222,6 +227,15 @@ def select_heads(p: Problem, scores, idx, stream=None) -> None:
                                   _stream(stream)), "dllm_select_heads")
 
 
+def refresh_select_attn(p: Problem, q, k_cache, v_cache, out, scores, idx, stream=None) -> None:
+    """dllm_refresh_select_attn: Refresh + Eq. 6 pool/TopK, the select fused into the Refresh kernel."""
+    bf = torch.bfloat16
+    _check(_lib.dllm_refresh_select_attn(p.ref, _dev(q, "q", bf), _dev(k_cache, "k_cache", bf),
+                                         _dev(v_cache, "v_cache", bf), _dev(out, "out", bf),
+                                         _dev(scores, "scores", torch.float32), _dev(idx, "idx", torch.int32),
+                                         _stream(stream)), "dllm_refresh_select_attn")
+
+
 def select_global(p: Problem, scores, idx, stream=None) -> None:
     """dllm_select_global (Eq. 5 uniform baseline: one shared set per request)."""
     _check(_lib.dllm_select_global(p.ref, _dev(scores, "scores", torch.float32), _dev(idx, "idx", torch.int32),
@@ -260,6 +274,17 @@ def mixed_attn(p_refresh: Problem, q, out, scores, p_reuse: Problem, q_blk, idx,
                                 _dev(scores, "scores", torch.float32), p_reuse.ref, _dev(q_blk, "q_blk", bf),
                                 _dev(idx, "idx", torch.int32), _dev(out_blk, "out_blk", bf), _dev(k_cache, "k_cache", bf),
                                 _dev(v_cache, "v_cache", bf), _stream(stream)), "dllm_mixed_attn")
+
+
+def mixed_select_attn(p_refresh: Problem, q, out, scores, idx_refresh, p_reuse: Problem, q_blk, idx, out_blk, k_cache,
+                      v_cache, stream=None) -> None:
+    """dllm_mixed_select_attn: mixed_attn with the Refresh requests' selection fused in."""
+    bf = torch.bfloat16
+    _check(_lib.dllm_mixed_select_attn(p_refresh.ref, _dev(q, "q", bf), _dev(out, "out", bf),
+                                       _dev(scores, "scores", torch.float32), _dev(idx_refresh, "idx_refresh", torch.int32),
+                                       p_reuse.ref, _dev(q_blk, "q_blk", bf), _dev(idx, "idx", torch.int32),
+                                       _dev(out_blk, "out_blk", bf), _dev(k_cache, "k_cache", bf),
+                                       _dev(v_cache, "v_cache", bf), _stream(stream)), "dllm_mixed_select_attn")
 
 
 def logit_chunks(n_logit: int, max_num_logits: int) -> list:
@@ -322,7 +347,6 @@ def alloc_buffers(p: Problem, device="cuda") -> Buffers:
 
 
 def hot_path(p: Problem, q, q_blk, k_cache, v_cache, buf: Buffers, stream=None) -> None:
-    """One pass of the whole hot path: Refresh (+importance) -> select -> Reuse."""
-    refresh_attn(p, q, k_cache, v_cache, buf.out, buf.scores, stream)
-    select_heads(p, buf.scores, buf.idx, stream)
+    """One pass of the whole hot path: Refresh (+importance, select fused in) -> Reuse."""
+    refresh_select_attn(p, q, k_cache, v_cache, buf.out, buf.scores, buf.idx, stream)
     reuse_sparse_attn(p, q_blk, k_cache, v_cache, buf.idx, buf.out_blk, stream)

@@ -49,6 +49,7 @@ def main():
         "refresh": lambda: lib.refresh_attn(p, q, kc, vc, buf.out, buf.scores),
         "select": lambda: lib.select_heads(p, buf.scores, buf.idx),
         "reuse": lambda: lib.reuse_sparse_attn(p, qb, kc, vc, buf.idx, buf.out_blk),
+        "refresh_select": lambda: lib.refresh_select_attn(p, q, kc, vc, buf.out, buf.scores, buf.idx),
     }
     k_, total_idx_, _, _ = p.layout()
     kp = torch.empty((max(total_idx_, 1), wl.head_dim), dtype=torch.bfloat16, device="cuda")
@@ -78,6 +79,9 @@ def main():
     print(f"{args.cfg} refresh: {t*1e6:.1f} us  {flops/t/1e12:.1f} TFLOP/s (min {res['refresh'][1]*1e6:.1f})")
     t = res["select"][0]
     print(f"{args.cfg} select : {t*1e6:.1f} us  {sel_bytes/t/1e9:.1f} GB/s")
+    t = res["refresh_select"][0]
+    print(f"{args.cfg} refresh+select fused: {t*1e6:.1f} us  {flops/t/1e12:.1f} TFLOP/s (Refresh FLOP; min "
+          f"{res['refresh_select'][1]*1e6:.1f})")
     t = res["reuse"][0]
     print(f"{args.cfg} reuse  : {t*1e6:.1f} us  {ub/t/1e9:.1f} GB/s unique ({lb/t/1e9:.1f} logical), "
           f"unique {ub/1e6:.1f} MB")

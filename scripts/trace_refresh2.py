@@ -14,10 +14,14 @@ p = lib.Problem(wl.seq_len, wl.blk_start, wl.blk_end, num_heads=wl.num_heads, nu
                 block_table=b.block_table.cuda())
 q, kc, vc = b.q.cuda(), b.k_cache.cuda(), b.v_cache.cuda()
 buf = lib.alloc_buffers(p)
+fused = len(sys.argv) > 2 and sys.argv[2] == "fused"
 for _ in range(3):
-    lib.refresh_attn(p, q, kc, vc, buf.out, buf.scores)
+    if fused:
+        lib.refresh_select_attn(p, q, kc, vc, buf.out, buf.scores, buf.idx)
+    else:
+        lib.refresh_attn(p, q, kc, vc, buf.out, buf.scores)
 torch.cuda.synchronize()
-tr = np.zeros((28, 512), dtype=np.int64)
+tr = np.zeros((34, 512), dtype=np.int64)
 lib.lib().dllm_trace2_read(tr.ctypes.data_as(ctypes.c_void_p))
 t0 = tr[0, 0]
 names = ["s0wait", "s1wait", "s0gotS", "s1gotS", "s0P", "s1P", "mWaitP0", "mGotP0", "mWaitP1", "mGotP1",
@@ -74,3 +78,12 @@ print("hist", [int(x) for x in hist[0]], [round(float(x), 0) for x in hist[1]])
 print("producer per step around the first two boundaries (abs - t0): K wait start, K got, V wait start, V got")
 for i in list(range(n_unit - 5, n_unit + 3)) + list(range(2 * n_unit - 3, 2 * n_unit + 2)):
     print(f"{i:4d} " + " ".join(f"{(tr[k, i] - t0):8d}" for k in (24, 25, 26, 27)))
+# softmax WG0 phase breakdown (clk): got S -> LDTM done -> max done -> exps done -> STTM waited -> P arrived
+N = 200
+ph = [tr[28, :N] - tr[2, :N], tr[29, :N] - tr[28, :N], tr[30, :N] - tr[29, :N], tr[31, :N] - tr[30, :N], tr[4, :N] - tr[31, :N]]
+print("softmax0 phases median (ld, importance+mask+max, rescale-check+exp, st+wait, fence+arrive):",
+      [float(np.median(x)) for x in ph])
+nsel = int((tr[33] > 0).sum())
+if nsel:
+    print("fused selects in CTA 0:", nsel, "durations (clk):", [int(x) for x in (tr[33, :nsel] - tr[32, :nsel])],
+          "start (clk from t0):", [int(x) for x in (tr[32, :nsel] - t0)])
