@@ -34,6 +34,7 @@ struct Plan {
   int32_t page_size, page_shift, pages_per_req;
   int32_t window;
   int32_t with_scores;  // refresh: also emit the Eq. 6 raw importance
+  int32_t sched_slot;   // refresh_tc2: dynamic unit scheduler counter slot (set per launch by the host)
   float scale_log2;  // tau * log2(e)
   float scale;       // tau
   const int32_t *block_table;

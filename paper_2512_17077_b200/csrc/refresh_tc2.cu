@@ -33,6 +33,8 @@
 #include <cudaTypedefs.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "plan.h"
 #include "tc_ptx.cuh"
@@ -96,6 +98,16 @@ constexpr bool kKVMerged = DLLM_TC2_KVMERGED;
 // polynomial on the FMA pipe instead of MUFU ex2 (16/clk/SM, the same rate at
 // which the tensor cores consume S elements at D = 128)
 constexpr int kPolyPairs = DLLM_TC2_POLY;
+#ifndef DLLM_TC2_DYNSCHED
+#define DLLM_TC2_DYNSCHED 1
+#endif
+// Dynamic unit scheduling: after its first (static) unit, a CTA claims the next
+// work unit from a device counter when its K/V producer needs it and publishes
+// the id to the other roles through a shared-memory ring, so CTAs that run
+// faster (fewer importance-epilogue units, less contended SMs) take more units.
+constexpr bool kDynSched = DLLM_TC2_DYNSCHED != 0;
+constexpr int kSchedSlots = 64;
+__device__ int g_tc2_sched[kSchedSlots][2];   // [slot]: {next unit - ncta, CTAs done}; self-resetting
 #ifndef DLLM_TC2_FUSEDSEL
 // 1: pool + TopK fused into the epilogue warpgroup (dllm_refresh_select_attn).  Off by
 // default: measured ~13 us per (b, h) selection at C1 (~25k clk, issue-starved beside
@@ -132,8 +144,13 @@ enum : int {
   B_OFULL = B_ODONE + 4,       // [tile]: last P.V of the unit completed
   B_OFREE = B_OFULL + 2,       // [tile]: epilogue has read O out of TMEM
   B_LFULL = B_OFREE + 2,       // [tile]: softmax row sums of the unit in smem
-  B_TMEMSLOT = B_LFULL + 2
+  B_TMEMSLOT = B_LFULL + 2,
+  B_RFULL = B_TMEMSLOT + 1,    // [kRing]: unit id published by the K/V producer (dynamic scheduler)
+  B_REMPTY = B_RFULL + 4       // [kRing]: read by every other role (kRingReaders arrivals)
 };
+constexpr int kRing = 4;
+constexpr int kRingReaders = 1 /* Q producer */ + 1 /* MMA warp */ + 8 /* softmax warps */ + 4 /* epilogue warps */;
+constexpr int kRingOff = 768;  // byte offset of the int ring[kRing] inside the barrier area
 __host__ __device__ constexpr uint32_t tmem_s(int tile, int buf) { return (uint32_t)(tile * 128 + buf * 64); }
 __host__ __device__ constexpr uint32_t tmem_o(int tile) { return tile ? 384u : 256u; }
 
@@ -408,6 +425,10 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
       ptx::mbar_init(bar(B_OFREE + i), 4);
       ptx::mbar_init(bar(B_LFULL + i), 4);
     }
+    for (int i = 0; i < kRing; ++i) {
+      ptx::mbar_init(bar(B_RFULL + i), 1);
+      ptx::mbar_init(bar(B_REMPTY + i), kRingReaders);
+    }
     ptx::mbar_init(bar(B_VZ), 1);
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&tm_q);
@@ -434,6 +455,20 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t *>(gb + C::kOffBar + 8 * B_TMEMSLOT);
+  static_assert(!(kDynSched && (kNextDecode || kL2Prefetch)), "next-unit options assume the static unit order");
+  volatile int *ring = reinterpret_cast<volatile int *>(gb + C::kOffBar + kRingOff);
+  // i-th unit of this CTA as seen by a reader role (static: cta + i * ncta).  A whole
+  // warp reads the slot and lane 0 releases it after __syncwarp; a single-thread
+  // role (the Q producer) reads and releases it alone.
+  auto unit_at = [&](int i, bool whole_warp) -> int {
+    if (!kDynSched) return cta + i * ncta;
+    const int slot = i % kRing;
+    ptx::mbar_wait(bar(B_RFULL + slot), (i / kRing) & 1);
+    const int u = ring[slot];
+    if (whole_warp) __syncwarp();
+    if (!whole_warp || lane == 0) ptx::mbar_arrive(bar(B_REMPTY + slot));
+    return u;
+  };
 
   if (warp == kProducerWarp) {
     // ============================ TMA producer ============================
@@ -445,7 +480,21 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
     // the next unit is decoded mid-unit (off the unit-boundary critical path)
     Unit un;
     if (cta < plan.total_units) decode_unit(plan, rs, cta, un, dcur);
-    for (int unit = cta; unit < plan.total_units; unit += ncta, ++ucnt) {
+    for (int i = 0;; ++i, ++ucnt) {
+      int unit = cta + i * ncta;
+      if (kDynSched) {
+        // this role needs the next unit first: claim it and publish it to the others
+        if (lane == 0) {
+          unit = i == 0 ? cta : ncta + atomicAdd(&g_tc2_sched[plan.sched_slot][0], 1);
+          unit = unit < plan.total_units ? unit : plan.total_units;
+          const int slot = i % kRing;
+          ptx::mbar_wait(bar(B_REMPTY + slot), ((i / kRing) & 1) ^ 1);
+          ring[slot] = unit;
+          ptx::mbar_arrive(bar(B_RFULL + slot));
+        }
+        unit = __shfl_sync(0xffffffffu, unit, 0);
+      }
+      if (unit >= plan.total_units) break;
       if (!kNextDecode) decode_unit(plan, rs, unit, un, dcur);
       const Unit u = un;
       const int32_t *bt = plan.block_table + (int64_t)u.bt_row * plan.pages_per_req;
@@ -540,7 +589,9 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
       int ucnt = 0;
       Unit un;
       if (cta < plan.total_units) decode_unit(plan, rs, cta, un, dcur);
-      for (int unit = cta; unit < plan.total_units; unit += ncta, ++ucnt) {
+      for (int i = 0;; ++i, ++ucnt) {
+        const int unit = unit_at(i, false);
+        if (unit >= plan.total_units) break;
         if (!kNextDecode) decode_unit(plan, rs, unit, un, dcur);
         const Unit u = un;
         if (kNextDecode && unit + ncta < plan.total_units) decode_unit(plan, rs, unit + ncta, un, dcur);
@@ -573,7 +624,9 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
       int ou[2] = {0, 0};        // units per Q tile (O accumulator reuse)
       Unit un;
       if (cta < plan.total_units) decode_unit(plan, rs, cta, un, dcur);
-      for (int unit = cta; unit < plan.total_units; unit += ncta, ++ucnt) {
+      for (int i = 0;; ++i, ++ucnt) {
+        const int unit = unit_at(i, true);
+        if (unit >= plan.total_units) break;
         if (lane == 0) TRACE2(23, 2 * ucnt);
         if (!kNextDecode) decode_unit(plan, rs, unit, un, dcur);
         const Unit u = un;
@@ -674,7 +727,9 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
     float *sbuf = reinterpret_cast<float *>(gb + C::kOffSc) + wg * (2 * 4 * TBN);
     const float sl2 = plan.scale_log2;
     int sc = 0, oc = 0;
-    for (int unit = cta; unit < plan.total_units; unit += ncta) {
+    for (int i = 0;; ++i) {
+      const int unit = unit_at(i, true);
+      if (unit >= plan.total_units) break;
       Unit u;
       decode_unit(plan, rs, unit, u, dcur);
       if (wg == 1 && !u.tile1) continue;
@@ -833,7 +888,9 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
     int oc[2] = {0, 0};
     int selc = 0;
     (void)selc;
-    for (int unit = cta; unit < plan.total_units; unit += ncta) {
+    for (int i = 0;; ++i) {
+      const int unit = unit_at(i, true);
+      if (unit >= plan.total_units) break;
       Unit u;
       decode_unit(plan, rs, unit, u, dcur);
       for (int i = 0; i < (u.tile1 ? 2 : 1); ++i) {
@@ -913,6 +970,15 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
   }
 #endif
   if (warp == kMmaWarp) ptx::tmem_dealloc(tmem, 512);
+  if (kDynSched && threadIdx.x == 0) {
+    // the last CTA of the launch resets the counter for the next launch on this slot
+    // (every CTA's claims precede its increment: __syncthreads above + fence)
+    __threadfence();
+    if (atomicAdd(&g_tc2_sched[plan.sched_slot][1], 1) == ncta - 1) {
+      atomicExch(&g_tc2_sched[plan.sched_slot][0], 0);
+      atomicExch(&g_tc2_sched[plan.sched_slot][1], 0);
+    }
+  }
 }
 
 template <int D>
@@ -960,6 +1026,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
       fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
   }
   return fn;
+}
+
+// launches in flight at the same time (different streams) get different counter
+// slots; a CUDA graph replays its captured slot, stream-ordered with itself
+int next_sched_slot() {
+  static std::atomic<unsigned> seq{0};
+  return (int)(seq.fetch_add(1u, std::memory_order_relaxed) % (unsigned)kSchedSlots);
 }
 
 int num_sms() {
@@ -1023,7 +1096,10 @@ cudaError_t launch_d(const Plan &plan, const void *q, const void *k, const void 
   if (e != cudaSuccess) return e;
   const int grid = plan.total_units < num_sms() ? plan.total_units : num_sms();
   if (grid <= 0) return cudaSuccess;
-  return launch_pdl(refresh_tc2_kernel<D>, dim3(grid), dim3(THREADS), smem, st, plan, tq, tk, tv, to,
+  static thread_local Plan pl;   // + the scheduler slot of this launch
+  pl = plan;
+  pl.sched_slot = next_sched_slot();
+  return launch_pdl(refresh_tc2_kernel<D>, dim3(grid), dim3(THREADS), smem, st, pl, tq, tk, tv, to,
                     (__nv_bfloat16 *)out, scores, sel_idx);
 }
 
@@ -1040,7 +1116,10 @@ cudaError_t launch_mixed_tc(const Plan &rplan, const void *q, const void *k, con
   e = cudaFuncSetAttribute(mixed_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   if (grid <= 0) return cudaSuccess;
-  return launch_pdl(mixed_tc_kernel, dim3(grid), dim3(THREADS), smem, st, rplan, tq, tk, tv, to, (__nv_bfloat16 *)out,
+  static thread_local Plan rpl;
+  rpl = rplan;
+  rpl.sched_slot = next_sched_slot();
+  return launch_pdl(mixed_tc_kernel, dim3(grid), dim3(THREADS), smem, st, rpl, tq, tk, tv, to, (__nv_bfloat16 *)out,
                     scores, uplan, (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k, (const __nv_bfloat16 *)v,
                     idx, (__nv_bfloat16 *)out_blk, n_ref, sel_idx);
 }
