@@ -20,7 +20,11 @@
  * to void*, NULL = legacy default stream) and return without synchronising.
  * They are CUDA-graph capturable.  Validation is all-or-nothing: on any
  * error nothing is enqueued.  Faults inside a kernel surface at the caller's
- * next synchronisation.
+ * next synchronisation.  The tcgen05 Refresh kernel balances its work units
+ * through a library-owned device counter (one of 64 self-resetting slots,
+ * round-robin per launch): up to 64 Refresh / mixed launches may be in flight
+ * at once on different streams; one captured graph must not be replayed
+ * concurrently with itself.
  *
  * Layouts (all bf16 tensors 16-byte aligned, row-major, innermost last):
  *   q, out         [sum_b L_b, H, D]   packed varlen, request b at rows
