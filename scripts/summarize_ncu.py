@@ -40,7 +40,9 @@ for name, k in KERNELS.items():
     m = raw(rep)
     b = sum(float(m[x][0].replace(",", "")) * UNIT.get(m[x][1], 1) for x in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     traffic.setdefault(cfg, {})[name] = {"kernel": k, "dram_bytes_per_launch": b, "round": rnd,
-                                         "duration_us_under_ncu": float(m["gpu__time_duration.sum"][0].replace(",", ""))}
+                                         "duration_us_under_ncu": float(m["gpu__time_duration.sum"][0].replace(",", "")) *
+                                         {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(
+                                             m["gpu__time_duration.sum"][1], 1.0)}
     lines.append(f"## {name} (`{k}`)")
     for x in METRICS:
         if x in m:
