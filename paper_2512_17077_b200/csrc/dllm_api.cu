@@ -509,6 +509,7 @@ int mixed_impl(const dllm_problem *p_refresh, const void *q, void *out, float *s
   for (int b = 0; b < Bu; ++b)
     t_reu += H * (double)(p_reuse->blk_end[b] - p_reuse->blk_start[b] + lu.k[b]) * 4.0 * D / 5.0e12;
   const int nsm = num_sms_mixed();
+  if (const char *e = getenv("DLLM_MIXED_REFRESH_WEIGHT")) t_ref *= atof(e);   // dev: A/B of the SM split
   int n_ref = (int)(nsm * t_ref / (t_ref + t_reu) + 0.5);
   n_ref = n_ref < 1 ? 1 : (n_ref > nsm - 1 ? nsm - 1 : n_ref);
   if (n_ref > rp.total_units) n_ref = rp.total_units;

@@ -106,6 +106,12 @@ constexpr int kPolyPairs = DLLM_TC2_POLY;
 // the id to the other roles through a shared-memory ring, so CTAs that run
 // faster (fewer importance-epilogue units, less contended SMs) take more units.
 constexpr bool kDynSched = DLLM_TC2_DYNSCHED != 0;
+#ifndef DLLM_TC2_QPREFETCH
+// 1: claim one unit ahead and prefetch its Q tiles to L2 (measured 1-3% slower at
+// C1/C2: the early claim costs balance, and L2 prefetches compete with the loads)
+#define DLLM_TC2_QPREFETCH 0
+#endif
+constexpr bool kQPrefetch = kDynSched && DLLM_TC2_QPREFETCH != 0;
 constexpr int kSchedSlots = 64;
 __device__ int g_tc2_sched[kSchedSlots][2];   // [slot]: {next unit - ncta, CTAs done}; self-resetting
 #ifndef DLLM_TC2_FUSEDSEL
@@ -480,12 +486,31 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
     // the next unit is decoded mid-unit (off the unit-boundary critical path)
     Unit un;
     if (cta < plan.total_units) decode_unit(plan, rs, cta, un, dcur);
+    int nxt_claim = -1;   // kQPrefetch: the unit claimed one ahead
     for (int i = 0;; ++i, ++ucnt) {
       int unit = cta + i * ncta;
       if (kDynSched) {
         // this role needs the next unit first: claim it and publish it to the others
         if (lane == 0) {
-          unit = i == 0 ? cta : ncta + atomicAdd(&g_tc2_sched[plan.sched_slot][0], 1);
+          auto claim = [&]() {
+            const int c = ncta + atomicAdd(&g_tc2_sched[plan.sched_slot][0], 1);
+            return c < plan.total_units ? c : plan.total_units;
+          };
+          if (!kQPrefetch) {
+            unit = i == 0 ? cta : claim();
+          } else {
+            // claim one unit ahead and pull its Q tiles into L2 now: their TMA load
+            // (issued when this unit's Q buffers drain) then hits L2 instead of HBM
+            unit = i == 0 ? cta : nxt_claim;
+            nxt_claim = unit < plan.total_units ? claim() : plan.total_units;
+            if (nxt_claim < plan.total_units) {
+              Unit v;
+              decode_unit(plan, rs, nxt_claim, v, dcur2);
+              for (int t = 0; t < (v.tile1 ? 2 : 1); ++t)
+                for (int c = 0; c < C::kChunks; ++c)
+                  ptx::tma_prefetch_3d(&tm_q, c * 64, v.h, v.q_off + (t ? v.origin1 : v.origin0));
+            }
+          }
           unit = unit < plan.total_units ? unit : plan.total_units;
           const int slot = i % kRing;
           ptx::mbar_wait(bar(B_REMPTY + slot), ((i / kRing) & 1) ^ 1);
@@ -1119,8 +1144,11 @@ cudaError_t launch_mixed_tc(const Plan &rplan, const void *q, const void *k, con
   static thread_local Plan rpl;
   rpl = rplan;
   rpl.sched_slot = next_sched_slot();
+  static thread_local Plan upl;
+  upl = uplan;
+  upl.sched_slot = rtc::rtc_next_sched_slot();
   return launch_pdl(mixed_tc_kernel, dim3(grid), dim3(THREADS), smem, st, rpl, tq, tk, tv, to, (__nv_bfloat16 *)out,
-                    scores, uplan, (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k, (const __nv_bfloat16 *)v,
+                    scores, upl, (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k, (const __nv_bfloat16 *)v,
                     idx, (__nv_bfloat16 *)out_blk, n_ref, sel_idx);
 }
 

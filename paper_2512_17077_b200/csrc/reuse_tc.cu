@@ -49,7 +49,10 @@ cudaError_t launch_reuse_tc(const Plan &plan, const void *q_blk, const void *k_c
   if (e != cudaSuccess) return e;
   const int grid = plan.total_units < num_sms_tc() ? plan.total_units : num_sms_tc();
   if (grid <= 0) return cudaSuccess;
-  return launch_pdl(reuse_tc_kernel, dim3(grid), dim3(kTThreads), (size_t)kTBytes, st, plan,
+  static thread_local Plan pl;   // + this launch's scheduler slot
+  pl = plan;
+  pl.sched_slot = rtc_next_sched_slot();
+  return launch_pdl(reuse_tc_kernel, dim3(grid), dim3(kTThreads), (size_t)kTBytes, st, pl,
                     (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k_cache, (const __nv_bfloat16 *)v_cache, idx,
                     (__nv_bfloat16 *)out);
 }

@@ -36,6 +36,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "plan.h"
 #include "tc_ptx.cuh"
@@ -72,6 +74,20 @@ constexpr int kTChunk = 128;        // keys per ring stage (MMA M of S^T)
 constexpr int kTNS = DLLM_RTC_NS;
 constexpr bool kPvEarly = DLLM_RTC_PVEARLY != 0;
 constexpr bool kRollingPrefetch = DLLM_RTC_PREFETCH == 1;
+#ifndef DLLM_RTC_DYNSCHED
+#define DLLM_RTC_DYNSCHED 0
+#endif
+// Dynamic unit scheduling (as in refresh_tc2.cu): after its first unit a CTA claims
+// the next one from a device counter when its translator needs it (one unit ahead,
+// for the L2 prefetch) and publishes the id to the other roles through a
+// shared-memory ring.  Off: measured 5-8% slower at C1/C2 and 5% slower for the
+// C3 mixed launch than the static order (same box, scripts/ab_c3_dyn.sh), where
+// neighbouring CTAs work on neighbouring heads of one request at the same time.
+constexpr bool kRtcDyn = DLLM_RTC_DYNSCHED != 0;
+constexpr int kRtcRing = 4;
+constexpr int kRtcRingReaders = 6 /* loaders */ + 1 /* MMA */ + 4 /* softmax */ + 4 /* epilogue */;
+constexpr int kRtcSchedSlots = 64;
+static __device__ int g_rtc_sched[kRtcSchedSlots][2];   // {claims, CTAs done}; the last CTA resets
 constexpr int kTNT = 4;             // translation ring depth (chunks)
 constexpr int kTTG = 4;             // chunks translated per batch
 // Warp roles (16 warps; the warp schedulers favour the highest warp id among the
@@ -95,8 +111,9 @@ constexpr int kOffStage = kOffL + 2 * 4 * 32 * 4;      // output staging [32 row
 constexpr int kBtMax = 1024;                          // block-table entries cached in shared memory
 constexpr int kOffBt = kOffStage + kTRows * kTD * 2;  // [kBtMax] int32
 constexpr int kOffBar = kOffBt + kBtMax * 4;
-constexpr int kNumBars = 2 * kTNS + 2 * kTNT + 2 + 2 + 2 + 2 + 2 + 1 + 2 + 2 + 2 + 1;
-constexpr int kTBytes = kOffBar + 8 * kNumBars + 1024;   // + alignment slack
+constexpr int kNumBars = 2 * kTNS + 2 * kTNT + 2 + 2 + 2 + 2 + 2 + 1 + 2 + 2 + 2 + 1 + 2 * kRtcRing;
+constexpr int kOffRing = kOffBar + 8 * kNumBars;         // int ring[kRtcRing]: unit ids
+constexpr int kTBytes = kOffRing + 4 * kRtcRing + 1024;   // + alignment slack
 static_assert(kTBytes <= 227 * 1024, "reuse_tc shared memory");
 
 // TMEM columns: S^T double buffer (32 each), O^T double buffer (32 each)
@@ -226,6 +243,19 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
   const uint32_t b_ofree = b_ofull + 16;              // [2] epilogue warps (4): O^T and row sums consumed
   const uint32_t b_lfull = b_ofree + 16;              // [2] softmax warps (4): row sums written
   const uint32_t b_tslot = b_lfull + 16;              // TMEM base address slot
+  const uint32_t b_rfull = b_tslot + 8;               // [kRtcRing] translator: unit id published
+  const uint32_t b_rempty = b_rfull + 8 * kRtcRing;   // [kRtcRing] every reader warp
+  volatile int *ring = reinterpret_cast<volatile int *>(gb + kOffRing);
+  // i-th unit of this CTA for a reader warp (static: cta + i * ncta)
+  auto unit_at = [&](int i) -> int {
+    if (!kRtcDyn) return cta + i * ncta;
+    const int slot = i % kRtcRing;
+    ptx::mbar_wait(b_rfull + 8 * slot, (i / kRtcRing) & 1);
+    const int u = ring[slot];
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(b_rempty + 8 * slot);
+    return u;
+  };
   int32_t *offs = reinterpret_cast<int32_t *>(gb + kOffOffs);
 
 #ifdef DLLM_TRACE
@@ -257,6 +287,10 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
       ptx::mbar_init(b_lfull + 8 * i, 4);
     }
     ptx::mbar_init(b_pvdone, 1);
+    for (int i = 0; i < kRtcRing; ++i) {
+      ptx::mbar_init(b_rfull + 8 * i, 1);
+      ptx::mbar_init(b_rempty + 8 * i, kRtcRingReaders);
+    }
     ptx::fence_mbar_init();
   }
   if (warp == kMmaWarp) {
@@ -290,14 +324,35 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
     }
     int t = 0, bt_cached = -1;
     int *bts = reinterpret_cast<int *>(gb + kOffBt);
-    for (int unit = cta; unit < plan.total_units; unit += ncta) {
+    auto claim = [&]() -> int {   // next unit of this CTA (dynamic), capped at total_units
+      int c = 0;
+      if (lane == 0) c = ncta + atomicAdd(&g_rtc_sched[plan.sched_slot][0], 1);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      return c < plan.total_units ? c : plan.total_units;
+    };
+    int unit = cta;
+    int nxt = cta < plan.total_units ? (kRtcDyn ? claim() : cta + ncta) : plan.total_units;
+    for (int i = 0;; ++i) {
+      if (kRtcDyn) {
+        if (lane == 0) {
+          const int slot = i % kRtcRing;
+          ptx::mbar_wait(b_rempty + 8 * slot, ((i / kRtcRing) & 1) ^ 1);
+          ring[slot] = unit < plan.total_units ? unit : plan.total_units;
+          ptx::mbar_arrive(b_rfull + 8 * slot);
+        }
+        __syncwarp();
+      }
+      if (unit >= plan.total_units) break;
+      const int cur = unit;
+      unit = nxt;
+      if (nxt < plan.total_units) nxt = kRtcDyn ? claim() : nxt + ncta;
       TUnit u;
-      tdecode(plan, unit, u);
-      if (kRollingPrefetch && unit + ncta < plan.total_units) {
+      tdecode(plan, cur, u);
+      if (kRollingPrefetch && unit < plan.total_units) {
         // the next unit's index list and block-table row go to L2 while this one is
         // translated (warp-uniform lookup, one bulk prefetch each)
         TUnit v;
-        tdecode(plan, unit + ncta, v);
+        tdecode(plan, unit, v);
         if (lane == 0 && v.k > 0) {
           const uintptr_t a0 = reinterpret_cast<uintptr_t>(idx + v.idx_off) & ~uintptr_t(15);
           const uintptr_t a1 = (reinterpret_cast<uintptr_t>(idx + v.idx_off + v.k) + 15) & ~uintptr_t(15);
@@ -371,7 +426,9 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
     const int li = loader_index(warp);
     const int64_t HD = (int64_t)plan.H * D;
     int t = 0, qc = 0;
-    for (int unit = cta; unit < plan.total_units; unit += ncta, ++qc) {
+    for (int i = 0;; ++i, ++qc) {
+      const int unit = unit_at(i);
+      if (unit >= plan.total_units) break;
       TUnit u;
       tdecode(plan, unit, u);
       const int nchunks = (u.nk + kTChunk - 1) / kTChunk;
@@ -440,7 +497,9 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
       RTC_CHUNK(5, pv_t);
       if (pv_last) ptx::mma_commit_elect(b_ofull + 8 * pv_ob);
     };
-    for (int unit = cta; unit < plan.total_units; unit += ncta, ++uc) {
+    for (int i = 0;; ++i, ++uc) {
+      const int unit = unit_at(i);
+      if (unit >= plan.total_units) break;
       TUnit u;
       tdecode(plan, unit, u);
       const int nchunks = (u.nk + kTChunk - 1) / kTChunk;
@@ -500,7 +559,9 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
     float *lbuf = reinterpret_cast<float *>(gb + kOffL);
     const uint32_t lane_base = (uint32_t)(sw * 32) << 16;
     int t = 0, uc = 0;
-    for (int unit = cta; unit < plan.total_units; unit += ncta, ++uc) {
+    for (int i = 0;; ++i, ++uc) {
+      const int unit = unit_at(i);
+      if (unit >= plan.total_units) break;
       TUnit u;
       tdecode(plan, unit, u);
       const int nchunks = (u.nk + kTChunk - 1) / kTChunk;
@@ -615,7 +676,9 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
     const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
     const float *lbuf = reinterpret_cast<const float *>(gb + kOffL);
     int uc = 0;
-    for (int unit = cta; unit < plan.total_units; unit += ncta, ++uc) {
+    for (int i = 0;; ++i, ++uc) {
+      const int unit = unit_at(i);
+      if (unit >= plan.total_units) break;
       TUnit u;
       tdecode(plan, unit, u);
       const int ob = uc & 1;
@@ -659,6 +722,20 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
   __syncthreads();
   ptx::tc_fence_after();
   if (warp == kMmaWarp) ptx::tmem_dealloc(tmem, kTmemCols);
+  if (kRtcDyn && threadIdx.x == 0) {
+    // the last CTA of the launch resets this slot for the next launch that uses it
+    __threadfence();
+    if (atomicAdd(&g_rtc_sched[plan.sched_slot][1], 1) == ncta - 1) {
+      atomicExch(&g_rtc_sched[plan.sched_slot][0], 0);
+      atomicExch(&g_rtc_sched[plan.sched_slot][1], 0);
+    }
+  }
+}
+
+// per-launch counter slot of the dynamic scheduler (host)
+inline int rtc_next_sched_slot() {
+  static std::atomic<unsigned> seq{0};
+  return (int)(seq.fetch_add(1u, std::memory_order_relaxed) % (unsigned)kRtcSchedSlots);
 }
 
 }  // namespace rtc
