@@ -92,12 +92,17 @@ constexpr bool kNextDecode = DLLM_TC2_NEXTDECODE;  // decode the next unit mid-u
 // released after the step's P.V): one wait and one commit fewer per step
 constexpr bool kKVMerged = DLLM_TC2_KVMERGED;
 #ifndef DLLM_TC2_POLY
-#define DLLM_TC2_POLY 2   // 2 of 8 (A/B: 0 -> 2 is +2% at C1, +1% at C2; 3 is slower)
+#define DLLM_TC2_POLY 1   // 1 of 8 (A/B, one run each: 0 / 1 / 2 of 8 -> C1 972 / 1,002 / 973 TFLOP/s; 3 / 4 of 8
+                          // 987 / 935; 1 of 4 / 16, 3 of 16 and a different share per warpgroup all slower)
 #endif
 // of every 8 exponential pairs of the softmax, this many run as a degree-3
 // polynomial on the FMA pipe instead of MUFU ex2 (16/clk/SM, the same rate at
 // which the tensor cores consume S elements at D = 128)
 constexpr int kPolyPairs = DLLM_TC2_POLY;
+#ifndef DLLM_TC2_POLY_PERIOD
+#define DLLM_TC2_POLY_PERIOD 8   // ... of every DLLM_TC2_POLY_PERIOD pairs (power of two <= 32)
+#endif
+constexpr int kPolyPeriod = DLLM_TC2_POLY_PERIOD;
 #ifndef DLLM_TC2_DYNSCHED
 #define DLLM_TC2_DYNSCHED 1
 #endif
@@ -866,7 +871,7 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
           for (int c = 0; c < 32; ++c) {
             const uint64_t x = ffma2(pack_f32x2(s[2 * c], s[2 * c + 1]), sl2x2, negm);
             float p0, p1;
-            if ((c & 7) < kPolyPairs) {
+            if ((c & (kPolyPeriod - 1)) < kPolyPairs) {
               unpack_f32x2(exp2_poly2(x), p0, p1);          // FMA pipe
             } else {
               float x0, x1;
