@@ -609,12 +609,18 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
           // warp has read it here)
           const float mc = fmaxf(fmaxf(red[lane], red[32 + lane]), fmaxf(red[64 + lane], red[96 + lane]));
           float alpha[32];
+          if (c == 0) {
+            // a unit's first chunk: nothing accumulated yet, no rescale factors
 #pragma unroll
-          for (int n = 0; n < 32; ++n) {
-            const float mn = fmaxf(m_run[n], __shfl_sync(0xffffffffu, mc, n));
-            alpha[n] = fast_exp2(m_run[n] - mn);
-            m_run[n] = mn;
-            l_part[n] *= alpha[n];
+            for (int n = 0; n < 32; ++n) m_run[n] = __shfl_sync(0xffffffffu, mc, n);
+          } else {
+#pragma unroll
+            for (int n = 0; n < 32; ++n) {
+              const float mn = fmaxf(m_run[n], __shfl_sync(0xffffffffu, mc, n));
+              alpha[n] = fast_exp2(m_run[n] - mn);
+              m_run[n] = mn;
+              l_part[n] *= alpha[n];
+            }
           }
           if (c > 0) {
             // O^T of this unit holds chunks < c: wait for P.V(t-1), rescale its columns
