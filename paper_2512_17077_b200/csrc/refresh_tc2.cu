@@ -69,7 +69,10 @@ constexpr int TBM = 128;            // query rows per tile
 constexpr int TBN = 64;             // keys per step
 constexpr int NST = 4;              // K and V ring stages
 constexpr int THREADS = 512;
-constexpr float kRescaleLog2 = 8.0f;
+#ifndef DLLM_TC2_RESCALE
+#define DLLM_TC2_RESCALE 8
+#endif
+constexpr float kRescaleLog2 = (float)DLLM_TC2_RESCALE;   // lazy-rescale threshold (log2 units)
 #ifndef DLLM_TC2_PREFETCH
 #define DLLM_TC2_PREFETCH 0
 #endif
