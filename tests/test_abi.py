@@ -107,6 +107,7 @@ def test_validation_rejects_bad_problems():
         assert L.lib().dllm_refresh_attn(p.ref, None, None, None, None, None, None) == code, name
         assert L.lib().dllm_reuse_sparse_attn(p.ref, None, None, None, None, None, None) == code, name
         assert L.lib().dllm_select_heads(p.ref, None, None, None) == code, name
+        assert L.lib().dllm_refresh_select_attn(p.ref, None, None, None, None, None, None, None) == code, name
         assert L.last_error() != ""
     bad_blocks = [([10], [5], [5]), ([10], [-1], [3]), ([10], [2], [11]), ([0], [0], [1]), ([300], [0], [200])]
     for Ls, bs, be in bad_blocks:
@@ -117,6 +118,10 @@ def test_validation_rejects_bad_problems():
     p = _prob(wl)
     assert L.lib().dllm_refresh_attn(p.ref, None, None, None, None, None, None) == L.DLLM_ERR_INVALID_ARG
     assert L.lib().dllm_select_heads(p.ref, None, None, None) == L.DLLM_ERR_INVALID_ARG
+    # the one-call Refresh + select requires both scores and idx
+    assert L.lib().dllm_refresh_select_attn(p.ref, None, None, None, None, None, None, None) == L.DLLM_ERR_INVALID_ARG
+    assert L.lib().dllm_mixed_select_attn(p.ref, None, None, None, None, p.ref, None, None, None, None, None,
+                                          None) == L.DLLM_ERR_INVALID_ARG
     # misaligned bf16 pointers
     base = q.data_ptr()
     assert L.lib().dllm_refresh_attn(p.ref, base + 2, base, base, base, None, None) == L.DLLM_ERR_SHAPE
