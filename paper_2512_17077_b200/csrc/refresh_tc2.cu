@@ -115,11 +115,14 @@ constexpr int kPolyPeriod = DLLM_TC2_POLY_PERIOD;
 // faster (fewer importance-epilogue units, less contended SMs) take more units.
 constexpr bool kDynSched = DLLM_TC2_DYNSCHED != 0;
 #ifndef DLLM_TC2_QPREFETCH
-// 1: claim one unit ahead and prefetch its Q tiles to L2 (measured 1-3% slower at
-// C1/C2: the early claim costs balance, and L2 prefetches compete with the loads)
+// N > 0: the K/V producer claims the next unit N steps before the current one ends
+// and prefetches its Q tiles into L2, so their TMA load at the unit boundary (issued
+// when this unit's Q buffers drain) hits L2.  (Claiming a whole unit ahead was
+// measured 1-3% slower at C1/C2.)
 #define DLLM_TC2_QPREFETCH 0
 #endif
 constexpr bool kQPrefetch = kDynSched && DLLM_TC2_QPREFETCH != 0;
+constexpr int kQPreSteps = DLLM_TC2_QPREFETCH;
 constexpr int kSchedSlots = 64;
 __device__ int g_tc2_sched[kSchedSlots][2];   // [slot]: {next unit - ncta, CTAs done}; self-resetting
 #ifndef DLLM_TC2_FUSEDSEL
@@ -494,31 +497,18 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
     // the next unit is decoded mid-unit (off the unit-boundary critical path)
     Unit un;
     if (cta < plan.total_units) decode_unit(plan, rs, cta, un, dcur);
-    int nxt_claim = -1;   // kQPrefetch: the unit claimed one ahead
+    int nxt_claim = -1;   // kQPrefetch: the next unit, claimed kQPreSteps steps before this one ends
+    auto claim = [&]() {
+      const int c = ncta + atomicAdd(&g_tc2_sched[plan.sched_slot][0], 1);
+      return c < plan.total_units ? c : plan.total_units;
+    };
     for (int i = 0;; ++i, ++ucnt) {
       int unit = cta + i * ncta;
       if (kDynSched) {
         // this role needs the next unit first: claim it and publish it to the others
         if (lane == 0) {
-          auto claim = [&]() {
-            const int c = ncta + atomicAdd(&g_tc2_sched[plan.sched_slot][0], 1);
-            return c < plan.total_units ? c : plan.total_units;
-          };
-          if (!kQPrefetch) {
-            unit = i == 0 ? cta : claim();
-          } else {
-            // claim one unit ahead and pull its Q tiles into L2 now: their TMA load
-            // (issued when this unit's Q buffers drain) then hits L2 instead of HBM
-            unit = i == 0 ? cta : nxt_claim;
-            nxt_claim = unit < plan.total_units ? claim() : plan.total_units;
-            if (nxt_claim < plan.total_units) {
-              Unit v;
-              decode_unit(plan, rs, nxt_claim, v, dcur2);
-              for (int t = 0; t < (v.tile1 ? 2 : 1); ++t)
-                for (int c = 0; c < C::kChunks; ++c)
-                  ptx::tma_prefetch_3d(&tm_q, c * 64, v.h, v.q_off + (t ? v.origin1 : v.origin0));
-            }
-          }
+          unit = i == 0 ? cta : (nxt_claim >= 0 ? nxt_claim : claim());
+          nxt_claim = -1;
           unit = unit < plan.total_units ? unit : plan.total_units;
           const int slot = i % kRing;
           ptx::mbar_wait(bar(B_REMPTY + slot), ((i / kRing) & 1) ^ 1);
@@ -562,6 +552,16 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
       for (int j = 0; j < u.n; ++j, ++it) {
         const int s = it % NST;
         const uint32_t ph = (it / NST) & 1;
+        if (kQPrefetch && lane == 0 && nxt_claim < 0 && j == (u.n > kQPreSteps ? u.n - kQPreSteps : 0)) {
+          nxt_claim = claim();
+          if (nxt_claim < plan.total_units) {
+            Unit v;
+            decode_unit(plan, rs, nxt_claim, v, dcur2);
+            for (int t = 0; t < (v.tile1 ? 2 : 1); ++t)
+              for (int c = 0; c < C::kChunks; ++c)
+                ptx::tma_prefetch_3d(&tm_q, c * 64, v.h, v.q_off + (t ? v.origin1 : v.origin0));
+          }
+        }
         const int key_end = min(TBN, u.L - j * TBN);      // valid keys in this step
         if (lane == 0) {
           int nvalid = 0;
