@@ -67,7 +67,10 @@ namespace {
 
 constexpr int TBM = 128;            // query rows per tile
 constexpr int TBN = 64;             // keys per step
-constexpr int NST = 4;              // K and V ring stages
+#ifndef DLLM_TC2_NST
+#define DLLM_TC2_NST 4
+#endif
+constexpr int NST = DLLM_TC2_NST;   // K and V ring stages
 constexpr int THREADS = 512;
 #ifndef DLLM_TC2_RESCALE
 #define DLLM_TC2_RESCALE 8
