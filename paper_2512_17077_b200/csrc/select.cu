@@ -26,7 +26,18 @@ namespace dllm {
 #endif
 constexpr int kSelThreads = DLLM_SEL_THREADS;
 constexpr int kSelWarps = kSelThreads / 32;
-constexpr int kSelSmemStageMax = 24576;   // words of dynamic smem for staged raw scores + keys (96 KB)
+constexpr int kSelSmemStageMax = 24576;
+#ifdef DLLM_TRACE
+// dev: phase timestamps (clock64) of a few CTAs: [cta][0 start, 1 after wait, 2 request found,
+// 3 raw staged, 4 pooled, 5..8 radix passes, 9 compaction done]
+__device__ long long g_sel_tr[8][10];
+extern "C" __attribute__((visibility("default"))) int dllm_trace_sel_read(long long *h) {
+  return (int)cudaMemcpyFromSymbol(h, g_sel_tr, sizeof(g_sel_tr));
+}
+#define SEL_TR(k) do { if (threadIdx.x == 0 && blockIdx.x < 8) g_sel_tr[blockIdx.x][k] = clock64(); } while (0)
+#else
+#define SEL_TR(k) do { } while (0)
+#endif   // words of dynamic smem for staged raw scores + keys (96 KB)
 
 __device__ __forceinline__ uint32_t order_key(float f) {
   uint32_t u = __float_as_uint(f);
@@ -71,7 +82,9 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
   __shared__ uint32_t s_prefix;
   __shared__ int s_krem;
 
+  SEL_TR(0);
   pdl_wait_then_trigger();
+  SEL_TR(1);
   const int unit = blockIdx.x;
   const int b = plan_find(plan, unit);
   const ReqInfo &R = plan.r[b];
@@ -83,6 +96,7 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
   const float *raw = scores + R.score_off + (int64_t)h * L;
   int32_t *out = idx + R.idx_off + (int64_t)h * k;
   const int half = plan.window >> 1;
+  SEL_TR(2);
 
   // 1. pool on the compacted axis, to order keys.  When the candidates fit twice in
   // shared memory, the raw scores are first staged there with all loads of a thread
@@ -93,6 +107,7 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
 #pragma unroll 4
     for (int c = threadIdx.x; c < n; c += kSelThreads) rawc[c] = __ldg(raw + (c < bs ? c : c + blk));
     __syncthreads();
+    SEL_TR(3);
     for (int c = threadIdx.x; c < n; c += kSelThreads) {
       const int lo = max(0, c - half), hi = min(n - 1, c + half);
       float m = -INFINITY;
@@ -112,6 +127,7 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
   }
   if (threadIdx.x == 0) { s_prefix = 0u; s_krem = k; }
   __syncthreads();
+  SEL_TR(4);
 
   // 2. radix select of the k-th largest key (MSB first)
   uint32_t prefix = 0u, mask = 0u;
@@ -165,6 +181,7 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
     krem = s_krem;
     mask |= 0xffu << shift;
     __syncthreads();
+    SEL_TR(5 + (24 - shift) / 8);
   }
   const uint32_t thr = prefix;   // exact key of the k-th largest
   const int need_eq = krem;      // how many keys equal to thr are taken (lowest index first)
@@ -186,6 +203,7 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
     gt_base += tot & 0xffff;
     eq_base += tot >> 16;
   }
+  SEL_TR(9);
 }
 
 // Uniform (global) selection, the Sparse-dLLM baseline of PAPER.md:136-145
