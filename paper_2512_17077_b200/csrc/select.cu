@@ -77,18 +77,20 @@ __global__ void __launch_bounds__(kSelThreads)
 select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__ scores,
                     int32_t *__restrict__ idx) {
   extern __shared__ uint32_t keys[];                  // [n_ctx]
-  __shared__ int hist[256];
+  __shared__ int hist[2][256];      // double-buffered: the next pass's is cleared while this one fills
   __shared__ int warp_buf[32];
-  __shared__ uint32_t s_prefix;
-  __shared__ int s_krem;
+  __shared__ uint32_t s_prefix[2];
+  __shared__ int s_krem[2];
 
   SEL_TR(0);
   pdl_wait_then_trigger();
   SEL_TR(1);
   const int unit = blockIdx.x;
-  const int b = plan_find(plan, unit);
+  // every request owns exactly H units (one per head): no search over the plan
+  // (a binary search in parameter memory cost ~1,200 clk of a ~14k clk CTA at C1)
+  const int b = unit / plan.H;
   const ReqInfo &R = plan.r[b];
-  const int h = unit - R.unit_off;
+  const int h = unit - b * plan.H;
   const int L = R.L, bs = R.bs, blk = R.be - R.bs;
   const int n = L - blk;
   const int k = R.k;
@@ -125,7 +127,7 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
       keys[c] = order_key(m);
     }
   }
-  if (threadIdx.x == 0) { s_prefix = 0u; s_krem = k; }
+  for (int i = threadIdx.x; i < 256; i += kSelThreads) hist[0][i] = 0;
   __syncthreads();
   SEL_TR(4);
 
@@ -134,8 +136,11 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
   int krem = k;
 #pragma unroll 1
   for (int shift = 24; shift >= 0; shift -= 8) {
-    for (int i = threadIdx.x; i < 256; i += kSelThreads) hist[i] = 0;
-    __syncthreads();
+    // two block barriers per pass: hist[cur] fills while hist[cur ^ 1] (read by the
+    // previous pass before its second barrier) is cleared for the next pass; the
+    // digit goes through s_prefix[cur], next rewritten two passes later
+    const int cur = ((24 - shift) >> 3) & 1;
+    for (int i = threadIdx.x; i < 256; i += kSelThreads) hist[cur ^ 1][i] = 0;
     // warp-aggregated: the candidates' keys crowd a few bins (similar exponents), so
     // lanes with equal bins are merged (match.any) into one shared atomic
     for (int c0 = 0; c0 < n; c0 += kSelThreads) {
@@ -144,7 +149,7 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
       const bool act = c < n && (key & mask) == prefix;
       const uint32_t bin = act ? ((key >> shift) & 0xffu) : 0x100u;
       const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-      if (act && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
+      if (act && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[cur][bin], __popc(peers));
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -153,7 +158,7 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
       const int base = 8 * (31 - lane);
       int cnt[8], sum = 0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) { cnt[i] = hist[base + 7 - i]; sum += cnt[i]; }  // descending bins
+      for (int i = 0; i < 8; ++i) { cnt[i] = hist[cur][base + 7 - i]; sum += cnt[i]; }  // descending bins
       int incl = sum;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -168,8 +173,8 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
         for (int i = 0; i < 8; ++i) {
           if (acc + cnt[i] >= krem) {
             const uint32_t digit = (uint32_t)(base + 7 - i);
-            s_prefix = prefix | (digit << shift);
-            s_krem = krem - acc;
+            s_prefix[cur] = prefix | (digit << shift);
+            s_krem[cur] = krem - acc;
             break;
           }
           acc += cnt[i];
@@ -177,10 +182,9 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
       }
     }
     __syncthreads();
-    prefix = s_prefix;
-    krem = s_krem;
+    prefix = s_prefix[cur];
+    krem = s_krem[cur];
     mask |= 0xffu << shift;
-    __syncthreads();
     SEL_TR(5 + (24 - shift) / 8);
   }
   const uint32_t thr = prefix;   // exact key of the k-th largest
