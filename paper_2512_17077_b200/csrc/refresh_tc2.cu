@@ -128,6 +128,10 @@ constexpr bool kQPrefetch = kDynSched && DLLM_TC2_QPREFETCH != 0;
 constexpr int kQPreSteps = DLLM_TC2_QPREFETCH;
 constexpr int kSchedSlots = 64;
 __device__ int g_tc2_sched[kSchedSlots][2];   // [slot]: {next unit - ncta, CTAs done}; self-resetting
+#ifndef DLLM_TC2_MMAPOLL
+#define DLLM_TC2_MMAPOLL 0   // 1: the MMA warp serves the two Q tiles in the order their P becomes ready
+#endif
+constexpr bool kMmaPoll = DLLM_TC2_MMAPOLL != 0;
 #ifndef DLLM_TC2_FUSEDSEL
 // 1: pool + TopK fused into the epilogue warpgroup (dllm_refresh_select_attn).  Off by
 // default: measured ~13 us per (b, h) selection at C1 (~25k clk, issue-starved beside
@@ -719,6 +723,7 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
           }
           const bool ahead = j + 2 < u.n;
           const int sk = (it + j + 2) % NST;
+          if (!kMmaPoll) {
           for (int i = 0; i < nt; ++i) {
             const int b = gp[i] & 1;
             if (lane == 0) TRACE2(6 + 2 * i, gp[i]);
@@ -739,6 +744,35 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
                 ptx::tc_fence_after();
               }
               qk(i, sk);
+            }
+          }
+          } else {
+            // whichever tile's P is ready first goes first (the two softmax warpgroups
+            // are not forced into lock-step by the issue order)
+            bool done[2] = {false, nt < 2};
+            bool kready = false;
+            while (!(done[0] && done[1])) {
+#pragma unroll
+              for (int i = 0; i < 2; ++i) {
+                if (done[i]) continue;
+                const int b = gp[i] & 1;
+                bool ready = ptx::mbar_test_wait(bar(B_PFULL + 2 * i + b), (gp[i] >> 1) & 1);
+                if (j == 0) ready = ready && ptx::mbar_test_wait(bar(B_OFREE + i), (ou[i] & 1) ^ 1);
+                ready = __shfl_sync(0xffffffffu, ready, 0);
+                if (!ready) continue;
+                if (j == 0) ++ou[i];
+                ptx::tc_fence_after();
+                pv(i, sv, j > 0, j == u.n - 1);
+                if (ahead) {
+                  if (!kready) {
+                    ptx::mbar_wait(bar(B_KFULL + sk), ((it + j + 2) / NST) & 1);
+                    ptx::tc_fence_after();
+                    kready = true;
+                  }
+                  qk(i, sk);
+                }
+                done[i] = true;
+              }
             }
           }
           if (ahead) {
