@@ -128,6 +128,13 @@ constexpr bool kQPrefetch = kDynSched && DLLM_TC2_QPREFETCH != 0;
 constexpr int kQPreSteps = DLLM_TC2_QPREFETCH;
 constexpr int kSchedSlots = 64;
 __device__ int g_tc2_sched[kSchedSlots][2];   // [slot]: {next unit - ncta, CTAs done}; self-resetting
+#ifndef DLLM_TC2_REG_SOFTMAX
+// register split (setmaxnreg): 8 softmax warps, 4 epilogue warps, 4 others at 64;
+// 2 * softmax + epilogue <= 448 for 64K registers per SM
+#define DLLM_TC2_REG_SOFTMAX 136
+#define DLLM_TC2_REG_EPI 176
+#endif
+static_assert(2 * DLLM_TC2_REG_SOFTMAX + DLLM_TC2_REG_EPI <= 448, "register budget");
 #ifndef DLLM_TC2_MMAPOLL
 #define DLLM_TC2_MMAPOLL 0   // 1: the MMA warp serves the two Q tiles in the order their P becomes ready
 #endif
@@ -788,7 +795,7 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
     __syncwarp();
   } else if (warp < 8) {
     // ============================ softmax warpgroups ============================
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 136;\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(DLLM_TC2_REG_SOFTMAX) : "memory");
     const int wg = warp >> 2;
     const int wq = warp & 3;                       // TMEM lane quarter
     const int row = wq * 32 + lane;                // row of the Q tile == TMEM lane
@@ -948,7 +955,7 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
     // Reads O_i out of TMEM as soon as the unit's last P.V completes, releases the
     // accumulator to the MMA warp, then normalises by the row sums and streams O to
     // global through the TMA store engine.  The softmax warps never wait for it.
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 176;\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(DLLM_TC2_REG_EPI) : "memory");
     const int wq = warp & 3;
     const int row = wq * 32 + lane;
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
