@@ -160,7 +160,7 @@ void fill_plan(Plan &pl, const dllm_problem *p, const std::vector<int32_t> &k, i
   pl.scale = scale_of(p);
   pl.scale_log2 = (float)((double)pl.scale * 1.4426950408889634);
   pl.block_table = p->block_table;
-  int u = 0;
+  int u = 0, upr = -1;
   for (int b = b0; b < b1; ++b) {
     ReqInfo &r = pl.r[b - b0];
     r.L = p->seq_len[b];
@@ -173,9 +173,12 @@ void fill_plan(Plan &pl, const dllm_problem *p, const std::vector<int32_t> &k, i
     r.score_off = (int64_t)p->num_heads * cu_L[b];
     r.unit_off = u;
     r.bt_row = b;
-    u += units(b);
+    const int ub = units(b);
+    upr = upr < 0 ? ub : (upr == ub ? upr : 0);
+    u += ub;
   }
   pl.total_units = u;
+  pl.units_per_req = upr > 0 ? upr : 0;
 }
 
 struct Layout {

@@ -35,6 +35,7 @@ struct Plan {
   int32_t window;
   int32_t with_scores;  // refresh: also emit the Eq. 6 raw importance
   int32_t sched_slot;   // refresh_tc2: dynamic unit scheduler counter slot (set per launch by the host)
+  int32_t units_per_req; // every request owns this many work units (0: they differ)
   float scale_log2;  // tau * log2(e)
   float scale;       // tau
   const int32_t *block_table;
@@ -44,6 +45,7 @@ struct Plan {
 #if defined(__CUDACC__)
 // Request owning work unit u: largest b with r[b].unit_off <= u.
 __device__ __forceinline__ int plan_find(const Plan &p, int u) {
+  if (p.units_per_req > 0) return u / p.units_per_req;   // uniform batch: no search
   int lo = 0, hi = p.nreq - 1;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;

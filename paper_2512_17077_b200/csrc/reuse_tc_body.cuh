@@ -348,9 +348,10 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
       if (nxt < plan.total_units) nxt = kRtcDyn ? claim() : nxt + ncta;
       TUnit u;
       tdecode(plan, cur, u);
-      if (kRollingPrefetch && unit < plan.total_units) {
-        // the next unit's index list and block-table row go to L2 while this one is
-        // translated (warp-uniform lookup, one bulk prefetch each)
+      // the next unit's index list and block-table row go to L2 while this one is
+      // translated (warp-uniform lookup, one bulk prefetch each); for the CTA's first
+      // unit only after its chunks are published (the lookup costs ~1k clk)
+      auto prefetch_next = [&]() {
         TUnit v;
         tdecode(plan, unit, v);
         if (lane == 0 && v.k > 0) {
@@ -365,7 +366,8 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
                                 15) & ~uintptr_t(15);
           ptx::bulk_prefetch_l2(reinterpret_cast<const void *>(b0), (uint32_t)(b1 - b0));
         }
-      }
+      };
+      if (kRollingPrefetch && unit < plan.total_units && i > 0) prefetch_next();
       const int32_t *my_idx = idx + u.idx_off;
       const int32_t *bt = plan.block_table + (int64_t)u.bt_row * plan.pages_per_req;
       const int nchunks = (u.nk + kTChunk - 1) / kTChunk;
@@ -419,6 +421,7 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
           ++t;
         }
       }
+      if (kRollingPrefetch && unit < plan.total_units && i == 0) prefetch_next();
     }
     cp_async_wait<0>();
   } else if (loader_index(warp) >= 0) {
