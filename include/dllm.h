@@ -20,11 +20,10 @@
  * to void*, NULL = legacy default stream) and return without synchronising.
  * They are CUDA-graph capturable.  Validation is all-or-nothing: on any
  * error nothing is enqueued.  Faults inside a kernel surface at the caller's
- * next synchronisation.  The tcgen05 Refresh kernel balances its work units
- * through a library-owned device counter (one of 64 self-resetting slots,
- * round-robin per launch): up to 64 Refresh / mixed launches may be in flight
- * at once on different streams; one captured graph must not be replayed
- * concurrently with itself.
+ * next synchronisation.  Device state of a launch (Reuse split-unit pieces,
+ * Refresh unit counters) lives only in the caller's optional workspace
+ * (dllm_problem.workspace); launches sharing one workspace must be
+ * stream-ordered.
  *
  * Layouts (all bf16 tensors 16-byte aligned, row-major, innermost last):
  *   q, out         [sum_b L_b, H, D]   packed varlen, request b at rows
@@ -71,6 +70,7 @@ extern "C" {
 #define DLLM_MAX_SEQ_LEN   65536   /* L_b upper bound for refresh / reuse            */
 #define DLLM_MAX_SELECT_LEN 32768  /* L_b upper bound for dllm_select_heads (smem)   */
 #define DLLM_MAX_BLOCK     128     /* blk_b = be_b - bs_b upper bound                */
+#define DLLM_MAX_POOL_WINDOW 65    /* pool_window upper bound (Table 3 uses 3)       */
 
 /* The problem statement of one batch (a packed batch
  * of requests with per-request sequence length and active-block position;
@@ -85,12 +85,28 @@ typedef struct dllm_problem {
   const int32_t *blk_start;    /* HOST [B]: 0 <= bs_b                             */
   const int32_t *blk_end;      /* HOST [B]: bs_b < be_b <= L_b, be-bs <= 128      */
   double keep_ratio;           /* r in (0, 1]                                     */
-  int32_t pool_window;         /* w odd >= 1 (Table 3 "Kernel Size" = 3)          */
+  int32_t pool_window;         /* w odd in [1, 65] (Table 3 "Kernel Size" = 3)    */
   float softmax_scale;         /* tau; 0 -> 1/sqrt(D) (Eq. 3/4 "sqrt(d)")         */
   int32_t page_size;           /* P: power of two in [16, 1024]                   */
   int32_t pages_per_req;       /* row stride of block_table, >= ceil(L_b / P)     */
   const int32_t *block_table;  /* DEVICE [B * pages_per_req] physical page ids    */
+  void *workspace;             /* DEVICE, optional (NULL ok): dllm_workspace_bytes()
+                                  bytes, 16-byte aligned, ZERO-initialised once by
+                                  the caller; every launch leaves it zeroed again.
+                                  It serialises the launches that use it: use one
+                                  workspace per stream (a captured graph must not be
+                                  replayed concurrently with another launch using
+                                  the same workspace).  With it, Reuse splits work
+                                  units across CTAs (equal work per SM, pieces merged
+                                  in-kernel) and Refresh claims its units from a
+                                  device counter; without it, Reuse keeps whole units
+                                  and Refresh uses a static round-robin schedule.   */
+  int64_t workspace_bytes;     /* size of `workspace` (>= dllm_workspace_bytes())  */
 } dllm_problem;
+
+/* Bytes of the optional DEVICE workspace of dllm_problem (a constant of the
+ * build, ~4.3 MB).  Host only. */
+DLLM_API int64_t dllm_workspace_bytes(void);
 
 /* k = ceil(r * n_ctx) in IEEE double, clamped to [1, n_ctx]; 0 if n_ctx == 0
  * ("k = L*r", R5).  Returns a negative status for

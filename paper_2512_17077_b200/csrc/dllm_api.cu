@@ -19,6 +19,7 @@
 
 #include "../../include/dllm.h"
 #include "plan.h"
+#include "workspace.h"
 
 namespace dllm {
 cudaError_t launch_select(const Plan &, const float *, int32_t *, cudaStream_t);
@@ -27,31 +28,27 @@ cudaError_t launch_select_global(const Plan &, const float *, int32_t *, cudaStr
 cudaError_t launch_reuse_packed(const Plan &, const void *, const void *, const void *, const void *, const void *,
                                 void *, cudaStream_t);
 cudaError_t launch_pack_kv(const Plan &, const void *, const void *, const int32_t *, void *, void *, cudaStream_t);
-cudaError_t launch_reuse(const Plan &, const void *, const void *, const void *, const int32_t *, void *,
-                         cudaStream_t);
 cudaError_t launch_refresh_mma(const Plan &, const void *, const void *, const void *, void *, float *,
                                cudaStream_t);
 cudaError_t launch_reuse_ws(const Plan &, const void *, const void *, const void *, const int32_t *, void *,
                             cudaStream_t);
 cudaError_t launch_mixed_tc(const Plan &rplan, const void *q, const void *k, const void *v, void *out, float *scores,
                             const Plan &uplan, const void *q_blk, const int32_t *idx, void *out_blk, int n_ref,
-                            int grid, int32_t *sel_idx, cudaStream_t st);
+                            int grid, int32_t *sel_idx, void *workspace, cudaStream_t st);
+int reuse_tc_grid(const Plan &plan, int max_ctas);
 int num_sms_mixed();
 int64_t lmhead_vocab_tiles(int vocab);
 cudaError_t launch_lmhead_chunk(const void *hidden, const void *weight, int n_tok, int d_model, int vocab, int row0,
                                 int n_rows, int32_t *ids, void *workspace, cudaStream_t st);
 bool reuse_tc_supported(int D);
 cudaError_t launch_reuse_tc(const Plan &, const void *, const void *, const void *, const int32_t *, void *,
-                            cudaStream_t);
+                            void *, cudaStream_t);
 int refresh_mma_units(int L, int bs, int be, int H, bool with_scores);
 bool refresh_tc_supported(int D);
 int refresh_tc2_units(int L, int bs, int be, int H, bool with_scores);
 cudaError_t launch_refresh_tc2(const Plan &, const void *, const void *, const void *, void *, float *, int32_t *,
                                cudaStream_t);
 int fused_select_max_n();
-int refresh_tc_units(int L, int bs, int be, int H, bool with_scores);
-cudaError_t launch_refresh_tc(const Plan &, const void *, const void *, const void *, void *, float *,
-                              cudaStream_t);
 }  // namespace dllm
 
 using namespace dllm;
@@ -104,6 +101,8 @@ int validate(const dllm_problem *p, std::vector<int32_t> *k) {
     return fail(DLLM_ERR_INVALID_ARG, "keep_ratio=%g not in (0,1]", p->keep_ratio);
   if (p->pool_window < 1 || (p->pool_window & 1) == 0)
     return fail(DLLM_ERR_INVALID_ARG, "pool_window=%d must be odd and >= 1", p->pool_window);
+  if (p->pool_window > DLLM_MAX_POOL_WINDOW)
+    return fail(DLLM_ERR_UNSUPPORTED, "pool_window=%d > %d", p->pool_window, DLLM_MAX_POOL_WINDOW);
   if (!(p->softmax_scale >= 0.f) || isinf(p->softmax_scale))
     return fail(DLLM_ERR_INVALID_ARG, "softmax_scale must be finite and >= 0 (0 = 1/sqrt(D))");
   const int P = p->page_size;
@@ -134,6 +133,9 @@ int validate(const dllm_problem *p, std::vector<int32_t> *k) {
     if (k) (*k)[b] = keep_count_impl(p->keep_ratio, L - (be - bs));
   }
   if (rows * p->num_heads * D > ((int64_t)1 << 40)) return fail(DLLM_ERR_UNSUPPORTED, "batch too large");
+  if (p->workspace && (((uintptr_t)p->workspace & 15u) || p->workspace_bytes < kWorkspaceBytes))
+    return fail(DLLM_ERR_INVALID_ARG, "workspace must be 16-byte aligned and hold dllm_workspace_bytes() = %lld bytes",
+                (long long)kWorkspaceBytes);
   return DLLM_OK;
 }
 
@@ -161,6 +163,7 @@ void fill_plan(Plan &pl, const dllm_problem *p, const std::vector<int32_t> &k, i
   pl.scale_log2 = (float)((double)pl.scale * 1.4426950408889634);
   pl.block_table = p->block_table;
   int u = 0, upr = -1;
+  int64_t cost = 0, rc = -1;
   for (int b = b0; b < b1; ++b) {
     ReqInfo &r = pl.r[b - b0];
     r.L = p->seq_len[b];
@@ -176,9 +179,16 @@ void fill_plan(Plan &pl, const dllm_problem *p, const std::vector<int32_t> &k, i
     const int ub = units(b);
     upr = upr < 0 ? ub : (upr == ub ? upr : 0);
     u += ub;
+    // Reuse balancing (plan.h): a unit of request b costs blk_b + k_b + kReuseUnitCost
+    r.cost_off = cost;
+    const int64_t c = (int64_t)ub * (r.be - r.bs + r.k + kReuseUnitCost);
+    rc = rc < 0 ? c : (rc == c ? rc : 0);
+    cost += c;
   }
   pl.total_units = u;
   pl.units_per_req = upr > 0 ? upr : 0;
+  pl.total_cost = cost;
+  pl.req_cost = (rc > 0 && rc <= INT32_MAX && upr > 0) ? (int32_t)rc : 0;
 }
 
 struct Layout {
@@ -207,27 +217,26 @@ int cuda_fail(cudaError_t e, const char *what) {
 }
 
 int reuse_impl_env() {
-  // DLLM_REUSE_IMPL=v1 | ws selects the one-CTA-per-unit mma.sync kernel or the
-  // persistent mma.sync kernel (A/B comparisons); default: tcgen05 (D = 128),
-  // else the persistent mma.sync kernel.
+  // DLLM_REUSE_IMPL=ws selects the persistent mma.sync kernel (A/B comparisons);
+  // default: tcgen05 (D = 128), else the persistent mma.sync kernel.
   const char *s = getenv("DLLM_REUSE_IMPL");
-  if (s && !strcmp(s, "v1")) return 0;
   if (s && !strcmp(s, "ws")) return 1;
   return 2;
 }
 
 int refresh_impl_env() {
-  // DLLM_REFRESH_IMPL=mma | tc1 selects the mma.sync kernel or the single-buffered
-  // tcgen05 kernel (A/B comparisons); default: tcgen05 with double-buffered S (tc2).
+  // DLLM_REFRESH_IMPL=mma selects the mma.sync kernel (A/B comparisons); default:
+  // tcgen05 (D = 64, 128), else the mma.sync kernel.
   const char *s = getenv("DLLM_REFRESH_IMPL");
   if (s && !strcmp(s, "mma")) return 0;
-  if (s && !strcmp(s, "tc1")) return 1;
   return 2;
 }
 
 }  // namespace
 
 extern "C" {
+
+int64_t dllm_workspace_bytes(void) { return kWorkspaceBytes; }
 
 int dllm_keep_count(double keep_ratio, int32_t n_ctx) {
   const int k = keep_count_impl(keep_ratio, n_ctx);
@@ -273,14 +282,11 @@ int refresh_impl(const dllm_problem *p, const void *q, const void *k_cache, cons
     const int b1 = b0 + kMaxReqPerLaunch < B ? b0 + kMaxReqPerLaunch : B;
     fill_plan(pl, p, lay.k, b0, b1, lay.cu_L, lay.cu_blk, lay.cu_k, [&](int b) {
       const int L = p->seq_len[b], bs = p->blk_start[b], be = p->blk_end[b], H = p->num_heads;
-      return impl == 2 ? refresh_tc2_units(L, bs, be, H, with_scores)
-             : impl == 1 ? refresh_tc_units(L, bs, be, H, with_scores)
-                         : refresh_mma_units(L, bs, be, H, with_scores);
+      return impl == 2 ? refresh_tc2_units(L, bs, be, H, with_scores) : refresh_mma_units(L, bs, be, H, with_scores);
     });
     pl.with_scores = with_scores;
     cudaError_t e = impl == 2 ? launch_refresh_tc2(pl, q, k_cache, v_cache, out, scores, sel_idx, s)
-                    : impl == 1 ? launch_refresh_tc(pl, q, k_cache, v_cache, out, scores, s)
-                                : launch_refresh_mma(pl, q, k_cache, v_cache, out, scores, s);
+                              : launch_refresh_mma(pl, q, k_cache, v_cache, out, scores, s);
     if (e != cudaSuccess) return cuda_fail(e, "refresh launch");
   }
   return ok();
@@ -382,11 +388,9 @@ int dllm_reuse_sparse_attn(const dllm_problem *p, const void *q_blk, const void 
       return p->num_heads * ((blk + 31) / 32);
     });
     const int impl = reuse_impl_env();
-    cudaError_t e =
-        impl == 2 && reuse_tc_supported(p->head_dim)
-            ? launch_reuse_tc(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream)
-        : impl >= 1 ? launch_reuse_ws(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream)
-                    : launch_reuse(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream);
+    cudaError_t e = impl == 2 && reuse_tc_supported(p->head_dim)
+                        ? launch_reuse_tc(pl, q_blk, k_cache, v_cache, idx, out_blk, p->workspace, (cudaStream_t)stream)
+                        : launch_reuse_ws(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "reuse launch");
   }
   return ok();
@@ -516,10 +520,9 @@ int mixed_impl(const dllm_problem *p_refresh, const void *q, void *out, float *s
   int n_ref = (int)(nsm * t_ref / (t_ref + t_reu) + 0.5);
   n_ref = n_ref < 1 ? 1 : (n_ref > nsm - 1 ? nsm - 1 : n_ref);
   if (n_ref > rp.total_units) n_ref = rp.total_units;
-  int n_reu = nsm - n_ref;
-  if (n_reu > up.total_units) n_reu = up.total_units;
+  const int n_reu = reuse_tc_grid(up, nsm - n_ref);
   cudaError_t e = launch_mixed_tc(rp, q, k_cache, v_cache, out, scores, up, q_blk, idx, out_blk, n_ref, n_ref + n_reu,
-                                  sel_idx, (cudaStream_t)stream);
+                                  sel_idx, p_reuse->workspace, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "mixed launch");
   return ok();
 }

@@ -25,6 +25,7 @@ struct ReqInfo {
   int64_t score_off; // H * cu_L[b]: first element in scores
   int32_t unit_off;  // prefix of work units (kernel specific) before this request
   int32_t bt_row;    // row of the block table (request index in the caller's batch)
+  int64_t cost_off;  // reuse: prefix of the work-unit costs (keys + kReuseUnitCost per unit) before this request
 };
 
 struct Plan {
@@ -36,11 +37,19 @@ struct Plan {
   int32_t with_scores;  // refresh: also emit the Eq. 6 raw importance
   int32_t sched_slot;   // refresh_tc2: dynamic unit scheduler counter slot (set per launch by the host)
   int32_t units_per_req; // every request owns this many work units (0: they differ)
+  int32_t req_cost;      // reuse: cost of every request when they are all equal (0: they differ)
+  int64_t total_cost;    // reuse: sum of the unit costs of the plan
   float scale_log2;  // tau * log2(e)
   float scale;       // tau
   const int32_t *block_table;
   ReqInfo r[kMaxReqPerLaunch];
 };
+
+// Reuse work balancing: a work unit (request, head, 32-row group) of nk = blk + k
+// keys costs nk + kReuseUnitCost "key equivalents" (its Q rows, its output rows and
+// the per-unit pipeline overheads); the launch's total cost is split evenly over
+// the CTAs (reuse_tc_body.cuh).
+constexpr int kReuseUnitCost = 32;
 
 #if defined(__CUDACC__)
 // Request owning work unit u: largest b with r[b].unit_off <= u.

@@ -39,6 +39,7 @@
 #include "plan.h"
 #include "tc_ptx.cuh"
 #include "reuse_tc_body.cuh"
+#include "workspace.h"
 
 #ifdef DLLM_TRACE
 __device__ long long g_trace2[34][512];
@@ -1083,13 +1084,15 @@ mixed_tc_kernel(const __grid_constant__ Plan rplan, const __grid_constant__ CUte
                 const __grid_constant__ Plan uplan, const __nv_bfloat16 *__restrict__ q_blk,
                 const __nv_bfloat16 *__restrict__ k_cache, const __nv_bfloat16 *__restrict__ v_cache,
                 const int32_t *__restrict__ idx, __nv_bfloat16 *__restrict__ out_blk, const int n_ref,
-                int32_t *__restrict__ sel_idx) {
-  pdl_wait_then_trigger();
-  if ((int)blockIdx.x < n_ref)
+                int32_t *__restrict__ sel_idx, float *__restrict__ ws_part, int32_t *__restrict__ ws_flags) {
+  if ((int)blockIdx.x < n_ref) {
+    pdl_wait_then_trigger();
     refresh_tc2_body<128>(rplan, tm_q, tm_k, tm_v, tm_o, out, scores, sel_idx, (int)blockIdx.x, n_ref);
-  else
-    rtc::reuse_tc_body(uplan, q_blk, k_cache, v_cache, idx, out_blk, (int)blockIdx.x - n_ref,
+  } else {
+    // (griddepcontrol.wait inside the body, after its input-independent prologue)
+    rtc::reuse_tc_body(uplan, q_blk, k_cache, v_cache, idx, out_blk, ws_part, ws_flags, (int)blockIdx.x - n_ref,
                        (int)gridDim.x - n_ref);
+  }
 }
 static_assert(THREADS == rtc::kTThreads, "mixed kernel: both bodies run 512-thread CTAs");
 
@@ -1184,7 +1187,7 @@ cudaError_t launch_d(const Plan &plan, const void *q, const void *k, const void 
 
 cudaError_t launch_mixed_tc(const Plan &rplan, const void *q, const void *k, const void *v, void *out, float *scores,
                             const Plan &uplan, const void *q_blk, const int32_t *idx, void *out_blk, int n_ref,
-                            int grid, int32_t *sel_idx, cudaStream_t st) {
+                            int grid, int32_t *sel_idx, void *workspace, cudaStream_t st) {
   if (rplan.D != 128 || uplan.D != 128) return cudaErrorInvalidValue;
   CUtensorMap tq, tk, tv, to;
   cudaError_t e = make_maps<128>(rplan, q, k, v, out, tq, tk, tv, to);
@@ -1196,15 +1199,17 @@ cudaError_t launch_mixed_tc(const Plan &rplan, const void *q, const void *k, con
   static thread_local Plan rpl;
   rpl = rplan;
   rpl.sched_slot = next_sched_slot();
-  static thread_local Plan upl;
-  upl = uplan;
-  upl.sched_slot = rtc::rtc_next_sched_slot();
+  float *ws_part = nullptr;
+  int32_t *ws_flags = nullptr;
+  workspace_split(workspace, ws_part, ws_flags);
   return launch_pdl(mixed_tc_kernel, dim3(grid), dim3(THREADS), smem, st, rpl, tq, tk, tv, to, (__nv_bfloat16 *)out,
-                    scores, upl, (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k, (const __nv_bfloat16 *)v,
-                    idx, (__nv_bfloat16 *)out_blk, n_ref, sel_idx);
+                    scores, uplan, (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k, (const __nv_bfloat16 *)v,
+                    idx, (__nv_bfloat16 *)out_blk, n_ref, sel_idx, ws_part, ws_flags);
 }
 
 int num_sms_mixed() { return num_sms(); }
+
+bool refresh_tc_supported(int D) { return D == 64 || D == 128; }
 
 int fused_select_max_n() { return DLLM_TC2_FUSEDSEL ? kFSelMaxN : 0; }
 

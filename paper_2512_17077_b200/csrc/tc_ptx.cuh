@@ -2,6 +2,9 @@
 // TMEM alloc / ld / st / commit / fences), UMMA descriptors.
 #pragma once
 #include <stdint.h>
+#ifdef DLLM_WATCHDOG
+#include <cstdio>
+#endif
 
 namespace dllm {
 namespace ptx {
@@ -38,10 +41,24 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
   return ok != 0;
 }
+#ifdef DLLM_WATCHDOG
+// dev builds (DLLM_VARIANT=DLLM_WATCHDOG): a wait that does not complete within
+// ~2^24 polls reports the barrier (smem offset), parity and thread, then traps
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t n = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    ++n;
+    if (n == (1u << 22) && (threadIdx.x & 31) == 0)
+      printf("WATCHDOG mbar 0x%x parity %u block %d thread %d\n", bar, parity, (int)blockIdx.x, (int)threadIdx.x);
+    if (n == (1u << 26)) __trap();
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+#endif
 
 // ---------------------------------------------------------------- fences / barriers
 __device__ __forceinline__ void fence_proxy_async_smem() {

@@ -26,7 +26,7 @@ DLLM_ERR_SHAPE = -3
 DLLM_ERR_K_RANGE = -4
 DLLM_ERR_CUDA = -5
 
-EXPORTED = ("dllm_keep_count", "dllm_index_layout", "dllm_refresh_attn", "dllm_select_heads", "dllm_select_global",
+EXPORTED = ("dllm_workspace_bytes", "dllm_keep_count", "dllm_index_layout", "dllm_refresh_attn", "dllm_select_heads", "dllm_select_global",
             "dllm_refresh_select_attn", "dllm_mixed_select_attn",
             "dllm_reuse_sparse_attn", "dllm_pack_kv", "dllm_reuse_packed", "dllm_mixed_attn", "dllm_logit_chunks",
             "dllm_lm_head_workspace_bytes", "dllm_lm_head_argmax", "dllm_check_indices", "dllm_status_string",
@@ -54,6 +54,8 @@ class _Problem(ctypes.Structure):
         ("page_size", ctypes.c_int32),
         ("pages_per_req", ctypes.c_int32),
         ("block_table", ctypes.c_void_p),
+        ("workspace", ctypes.c_void_p),
+        ("workspace_bytes", ctypes.c_int64),
     ]
 
 
@@ -64,6 +66,9 @@ def _load() -> ctypes.CDLL:
     lib = ctypes.CDLL(LIB_PATH)
     P = ctypes.POINTER(_Problem)
     vp = ctypes.c_void_p
+    if hasattr(lib, "dllm_workspace_bytes"):   # (absent in dev A/B builds of older sources)
+        lib.dllm_workspace_bytes.argtypes = []
+        lib.dllm_workspace_bytes.restype = ctypes.c_int64
     lib.dllm_keep_count.argtypes = [ctypes.c_double, ctypes.c_int32]
     lib.dllm_keep_count.restype = ctypes.c_int
     lib.dllm_index_layout.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64),
@@ -139,15 +144,33 @@ def _i32(xs) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(xs, dtype=np.int32))
 
 
+def workspace_bytes() -> int:
+    return int(_lib.dllm_workspace_bytes()) if hasattr(_lib, "dllm_workspace_bytes") else 16
+
+
+def alloc_workspace(device="cuda") -> torch.Tensor:
+    """A zeroed dllm_problem workspace (one per stream; it stays zeroed across launches)."""
+    return torch.zeros(workspace_bytes(), dtype=torch.uint8, device=device)
+
+
 class Problem:
-    """Owns the host arrays and the device block table behind a dllm_problem."""
+    """Owns the host arrays, the device block table and the workspace behind a dllm_problem.
+
+    workspace: "auto" (default) allocates a zeroed one on the block table's device,
+    None runs without (Reuse keeps whole units, Refresh schedules statically), or a
+    caller tensor of at least workspace_bytes() bytes."""
 
     def __init__(self, seq_len: Sequence[int], blk_start: Sequence[int], blk_end: Sequence[int], *,
                  num_heads: int, num_kv_heads: int, head_dim: int, keep_ratio: float, pool_window: int = 3,
                  softmax_scale: float = 0.0, page_size: int = 64, block_table: Optional[torch.Tensor] = None,
-                 pages_per_req: Optional[int] = None):
+                 pages_per_req: Optional[int] = None, workspace="auto"):
         self.seq_len, self.blk_start, self.blk_end = _i32(seq_len), _i32(blk_start), _i32(blk_end)
         self.block_table = block_table
+        if isinstance(workspace, str):
+            assert workspace == "auto"
+            workspace = (alloc_workspace(block_table.device) if block_table is not None and block_table.is_cuda
+                         else None)
+        self.workspace = workspace
         if pages_per_req is None:
             pages_per_req = int(block_table.shape[1]) if block_table is not None and block_table.dim() == 2 else 0
         self._s = _Problem()
@@ -168,6 +191,14 @@ class Problem:
             s.block_table = block_table.data_ptr()
         else:
             s.block_table = None
+        if workspace is not None:
+            if not (workspace.is_cuda and workspace.is_contiguous()):
+                raise ValueError("workspace must be a contiguous CUDA tensor")
+            s.workspace = workspace.data_ptr()
+            s.workspace_bytes = workspace.numel() * workspace.element_size()
+        else:
+            s.workspace, s.workspace_bytes = None, 0
+        self._layout = None
 
     @property
     def ref(self):
@@ -187,6 +218,11 @@ class Problem:
 
     def layout(self):
         """(k per request, total idx elements, total rows, total block rows)."""
+        if self._layout is None:
+            self._layout = self._query_layout()
+        return self._layout
+
+    def _query_layout(self):
         B = self._s.num_requests
         k = (ctypes.c_int32 * max(B, 1))()
         ti, tr, tb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
@@ -195,7 +231,7 @@ class Problem:
         return [k[i] for i in range(B)], ti.value, tr.value, tb.value
 
 
-def _dev(t: Optional[torch.Tensor], name: str, dtype=None) -> int:
+def _dev(t: Optional[torch.Tensor], name: str, dtype=None, need: int = 0) -> int:
     if t is None:
         return 0
     if not t.is_cuda:
@@ -204,7 +240,16 @@ def _dev(t: Optional[torch.Tensor], name: str, dtype=None) -> int:
         raise ValueError(f"{name} must be contiguous")
     if dtype is not None and t.dtype != dtype:
         raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if t.numel() < need:
+        raise ValueError(f"{name} holds {t.numel()} elements, the problem's layout needs {need}")
     return t.data_ptr()
+
+
+def _sizes(p: "Problem"):
+    """Element counts the layout needs: (q/out rows*H*D, scores H*rows, idx, q_blk/out_blk)."""
+    _, total_idx, rows, blk_rows = p.layout()
+    HD = p.num_heads * p.head_dim
+    return rows * HD, p.num_heads * rows, total_idx, blk_rows * HD
 
 
 def _stream(stream) -> int:
@@ -216,38 +261,43 @@ def _stream(stream) -> int:
 def refresh_attn(p: Problem, q, k_cache, v_cache, out, scores=None, stream=None) -> None:
     """dllm_refresh_attn (Eq. 3 + Eq. 6 raw importance)."""
     bf = torch.bfloat16
-    _check(_lib.dllm_refresh_attn(p.ref, _dev(q, "q", bf), _dev(k_cache, "k_cache", bf), _dev(v_cache, "v_cache", bf),
-                                  _dev(out, "out", bf), _dev(scores, "scores", torch.float32), _stream(stream)),
-           "dllm_refresh_attn")
+    nq, ns, _, _ = _sizes(p)
+    _check(_lib.dllm_refresh_attn(p.ref, _dev(q, "q", bf, nq), _dev(k_cache, "k_cache", bf),
+                                  _dev(v_cache, "v_cache", bf), _dev(out, "out", bf, nq),
+                                  _dev(scores, "scores", torch.float32, ns), _stream(stream)), "dllm_refresh_attn")
 
 
 def select_heads(p: Problem, scores, idx, stream=None) -> None:
     """dllm_select_heads (Eq. 6 pool + per-head TopK)."""
-    _check(_lib.dllm_select_heads(p.ref, _dev(scores, "scores", torch.float32), _dev(idx, "idx", torch.int32),
+    _, ns, ni, _ = _sizes(p)
+    _check(_lib.dllm_select_heads(p.ref, _dev(scores, "scores", torch.float32, ns), _dev(idx, "idx", torch.int32, ni),
                                   _stream(stream)), "dllm_select_heads")
 
 
 def refresh_select_attn(p: Problem, q, k_cache, v_cache, out, scores, idx, stream=None) -> None:
     """dllm_refresh_select_attn: Refresh + Eq. 6 pool/TopK, the select fused into the Refresh kernel."""
     bf = torch.bfloat16
-    _check(_lib.dllm_refresh_select_attn(p.ref, _dev(q, "q", bf), _dev(k_cache, "k_cache", bf),
-                                         _dev(v_cache, "v_cache", bf), _dev(out, "out", bf),
-                                         _dev(scores, "scores", torch.float32), _dev(idx, "idx", torch.int32),
+    nq, ns, ni, _ = _sizes(p)
+    _check(_lib.dllm_refresh_select_attn(p.ref, _dev(q, "q", bf, nq), _dev(k_cache, "k_cache", bf),
+                                         _dev(v_cache, "v_cache", bf), _dev(out, "out", bf, nq),
+                                         _dev(scores, "scores", torch.float32, ns), _dev(idx, "idx", torch.int32, ni),
                                          _stream(stream)), "dllm_refresh_select_attn")
 
 
 def select_global(p: Problem, scores, idx, stream=None) -> None:
     """dllm_select_global (Eq. 5 uniform baseline: one shared set per request)."""
-    _check(_lib.dllm_select_global(p.ref, _dev(scores, "scores", torch.float32), _dev(idx, "idx", torch.int32),
-                                   _stream(stream)), "dllm_select_global")
+    _, ns, ni, _ = _sizes(p)
+    _check(_lib.dllm_select_global(p.ref, _dev(scores, "scores", torch.float32, ns),
+                                   _dev(idx, "idx", torch.int32, ni), _stream(stream)), "dllm_select_global")
 
 
 def reuse_sparse_attn(p: Problem, q_blk, k_cache, v_cache, idx, out_blk, stream=None) -> None:
     """dllm_reuse_sparse_attn (Eq. 4 over per-head key subsets)."""
     bf = torch.bfloat16
-    _check(_lib.dllm_reuse_sparse_attn(p.ref, _dev(q_blk, "q_blk", bf), _dev(k_cache, "k_cache", bf),
-                                       _dev(v_cache, "v_cache", bf), _dev(idx, "idx", torch.int32),
-                                       _dev(out_blk, "out_blk", bf), _stream(stream)), "dllm_reuse_sparse_attn")
+    _, _, ni, nb = _sizes(p)
+    _check(_lib.dllm_reuse_sparse_attn(p.ref, _dev(q_blk, "q_blk", bf, nb), _dev(k_cache, "k_cache", bf),
+                                       _dev(v_cache, "v_cache", bf), _dev(idx, "idx", torch.int32, ni),
+                                       _dev(out_blk, "out_blk", bf, nb), _stream(stream)), "dllm_reuse_sparse_attn")
 
 
 def pack_kv(p: Problem, k_cache, v_cache, idx, k_pack, v_pack, stream=None) -> None:
@@ -270,20 +320,26 @@ def mixed_attn(p_refresh: Problem, q, out, scores, p_reuse: Problem, q_blk, idx,
                stream=None) -> None:
     """Refresh over p_refresh and Reuse over p_reuse in one launch (N3)."""
     bf = torch.bfloat16
-    _check(_lib.dllm_mixed_attn(p_refresh.ref, _dev(q, "q", bf), _dev(out, "out", bf),
-                                _dev(scores, "scores", torch.float32), p_reuse.ref, _dev(q_blk, "q_blk", bf),
-                                _dev(idx, "idx", torch.int32), _dev(out_blk, "out_blk", bf), _dev(k_cache, "k_cache", bf),
-                                _dev(v_cache, "v_cache", bf), _stream(stream)), "dllm_mixed_attn")
+    nq, ns, _, _ = _sizes(p_refresh)
+    _, _, ni, nb = _sizes(p_reuse)
+    _check(_lib.dllm_mixed_attn(p_refresh.ref, _dev(q, "q", bf, nq), _dev(out, "out", bf, nq),
+                                _dev(scores, "scores", torch.float32, ns), p_reuse.ref, _dev(q_blk, "q_blk", bf, nb),
+                                _dev(idx, "idx", torch.int32, ni), _dev(out_blk, "out_blk", bf, nb),
+                                _dev(k_cache, "k_cache", bf), _dev(v_cache, "v_cache", bf), _stream(stream)),
+           "dllm_mixed_attn")
 
 
 def mixed_select_attn(p_refresh: Problem, q, out, scores, idx_refresh, p_reuse: Problem, q_blk, idx, out_blk, k_cache,
                       v_cache, stream=None) -> None:
     """dllm_mixed_select_attn: mixed_attn with the Refresh requests' selection fused in."""
     bf = torch.bfloat16
-    _check(_lib.dllm_mixed_select_attn(p_refresh.ref, _dev(q, "q", bf), _dev(out, "out", bf),
-                                       _dev(scores, "scores", torch.float32), _dev(idx_refresh, "idx_refresh", torch.int32),
-                                       p_reuse.ref, _dev(q_blk, "q_blk", bf), _dev(idx, "idx", torch.int32),
-                                       _dev(out_blk, "out_blk", bf), _dev(k_cache, "k_cache", bf),
+    nq, ns, nir, _ = _sizes(p_refresh)
+    _, _, ni, nb = _sizes(p_reuse)
+    _check(_lib.dllm_mixed_select_attn(p_refresh.ref, _dev(q, "q", bf, nq), _dev(out, "out", bf, nq),
+                                       _dev(scores, "scores", torch.float32, ns),
+                                       _dev(idx_refresh, "idx_refresh", torch.int32, nir),
+                                       p_reuse.ref, _dev(q_blk, "q_blk", bf, nb), _dev(idx, "idx", torch.int32, ni),
+                                       _dev(out_blk, "out_blk", bf, nb), _dev(k_cache, "k_cache", bf),
                                        _dev(v_cache, "v_cache", bf), _stream(stream)), "dllm_mixed_select_attn")
 
 
