@@ -20,8 +20,8 @@
  * to void*, NULL = legacy default stream) and return without synchronising.
  * They are CUDA-graph capturable.  Validation is all-or-nothing: on any
  * error nothing is enqueued.  Faults inside a kernel surface at the caller's
- * next synchronisation.  Device state of a launch (Reuse split-unit pieces,
- * Refresh unit counters) lives only in the caller's optional workspace
+ * next synchronisation.  Device state of a launch (the Refresh unit
+ * counters) lives only in the caller's optional workspace
  * (dllm_problem.workspace); launches sharing one workspace must be
  * stream-ordered.
  *
@@ -93,19 +93,18 @@ typedef struct dllm_problem {
   void *workspace;             /* DEVICE, optional (NULL ok): dllm_workspace_bytes()
                                   bytes, 16-byte aligned, ZERO-initialised once by
                                   the caller; every launch leaves it zeroed again.
-                                  It serialises the launches that use it: use one
-                                  workspace per stream (a captured graph must not be
-                                  replayed concurrently with another launch using
-                                  the same workspace).  With it, Reuse splits work
-                                  units across CTAs (equal work per SM, pieces merged
-                                  in-kernel) and Refresh claims its units from a
-                                  device counter; without it, Reuse keeps whole units
-                                  and Refresh uses a static round-robin schedule.   */
+                                  It holds the Refresh kernel's dynamic work-unit
+                                  counters, so launches using one workspace must be
+                                  stream-ordered: one workspace per stream (a
+                                  captured graph must not be replayed concurrently
+                                  with another launch on the same workspace).
+                                  NULL: Refresh schedules its units statically
+                                  (round-robin; same results, slower tails).      */
   int64_t workspace_bytes;     /* size of `workspace` (>= dllm_workspace_bytes())  */
 } dllm_problem;
 
 /* Bytes of the optional DEVICE workspace of dllm_problem (a constant of the
- * build, ~4.3 MB).  Host only. */
+ * build, 4 KB).  Host only. */
 DLLM_API int64_t dllm_workspace_bytes(void);
 
 /* k = ceil(r * n_ctx) in IEEE double, clamped to [1, n_ctx]; 0 if n_ctx == 0

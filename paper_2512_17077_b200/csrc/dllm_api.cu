@@ -47,7 +47,7 @@ int refresh_mma_units(int L, int bs, int be, int H, bool with_scores);
 bool refresh_tc_supported(int D);
 int refresh_tc2_units(int L, int bs, int be, int H, bool with_scores);
 cudaError_t launch_refresh_tc2(const Plan &, const void *, const void *, const void *, void *, float *, int32_t *,
-                               cudaStream_t);
+                               void *, cudaStream_t);
 int fused_select_max_n();
 }  // namespace dllm
 
@@ -285,7 +285,7 @@ int refresh_impl(const dllm_problem *p, const void *q, const void *k_cache, cons
       return impl == 2 ? refresh_tc2_units(L, bs, be, H, with_scores) : refresh_mma_units(L, bs, be, H, with_scores);
     });
     pl.with_scores = with_scores;
-    cudaError_t e = impl == 2 ? launch_refresh_tc2(pl, q, k_cache, v_cache, out, scores, sel_idx, s)
+    cudaError_t e = impl == 2 ? launch_refresh_tc2(pl, q, k_cache, v_cache, out, scores, sel_idx, p->workspace, s)
                               : launch_refresh_mma(pl, q, k_cache, v_cache, out, scores, s);
     if (e != cudaSuccess) return cuda_fail(e, "refresh launch");
   }
@@ -522,7 +522,7 @@ int mixed_impl(const dllm_problem *p_refresh, const void *q, void *out, float *s
   if (n_ref > rp.total_units) n_ref = rp.total_units;
   const int n_reu = reuse_tc_grid(up, nsm - n_ref);
   cudaError_t e = launch_mixed_tc(rp, q, k_cache, v_cache, out, scores, up, q_blk, idx, out_blk, n_ref, n_ref + n_reu,
-                                  sel_idx, p_reuse->workspace, (cudaStream_t)stream);
+                                  sel_idx, p_refresh->workspace, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "mixed launch");
   return ok();
 }

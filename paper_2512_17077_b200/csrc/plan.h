@@ -35,13 +35,13 @@ struct Plan {
   int32_t page_size, page_shift, pages_per_req;
   int32_t window;
   int32_t with_scores;  // refresh: also emit the Eq. 6 raw importance
-  int32_t sched_slot;   // refresh_tc2: dynamic unit scheduler counter slot (set per launch by the host)
   int32_t units_per_req; // every request owns this many work units (0: they differ)
   int32_t req_cost;      // reuse: cost of every request when they are all equal (0: they differ)
   int64_t total_cost;    // reuse: sum of the unit costs of the plan
   float scale_log2;  // tau * log2(e)
   float scale;       // tau
   const int32_t *block_table;
+  int32_t *sched;        // refresh_tc2: {claims, CTAs done} unit counters in the caller's workspace, or NULL
   ReqInfo r[kMaxReqPerLaunch];
 };
 

@@ -127,8 +127,6 @@ constexpr bool kDynSched = DLLM_TC2_DYNSCHED != 0;
 #endif
 constexpr bool kQPrefetch = kDynSched && DLLM_TC2_QPREFETCH != 0;
 constexpr int kQPreSteps = DLLM_TC2_QPREFETCH;
-constexpr int kSchedSlots = 64;
-__device__ int g_tc2_sched[kSchedSlots][2];   // [slot]: {next unit - ncta, CTAs done}; self-resetting
 #ifndef DLLM_TC2_REG_SOFTMAX
 // register split (setmaxnreg): 8 softmax warps, 4 epilogue warps, 4 others at 64;
 // 2 * softmax + epilogue <= 448 for 64K registers per SM
@@ -488,12 +486,15 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
   ptx::tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t *>(gb + C::kOffBar + 8 * B_TMEMSLOT);
   static_assert(!(kDynSched && (kNextDecode || kL2Prefetch)), "next-unit options assume the static unit order");
+  // the device counter lives in the caller's workspace (dllm_problem.workspace):
+  // without one the units go round-robin
+  const bool dyn = kDynSched && plan.sched != nullptr;
   volatile int *ring = reinterpret_cast<volatile int *>(gb + C::kOffBar + kRingOff);
   // i-th unit of this CTA as seen by a reader role (static: cta + i * ncta).  A whole
   // warp reads the slot and lane 0 releases it after __syncwarp; a single-thread
   // role (the Q producer) reads and releases it alone.
   auto unit_at = [&](int i, bool whole_warp) -> int {
-    if (!kDynSched) return cta + i * ncta;
+    if (!dyn) return cta + i * ncta;
     const int slot = i % kRing;
     ptx::mbar_wait(bar(B_RFULL + slot), (i / kRing) & 1);
     const int u = ring[slot];
@@ -514,12 +515,12 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
     if (cta < plan.total_units) decode_unit(plan, rs, cta, un, dcur);
     int nxt_claim = -1;   // kQPrefetch: the next unit, claimed kQPreSteps steps before this one ends
     auto claim = [&]() {
-      const int c = ncta + atomicAdd(&g_tc2_sched[plan.sched_slot][0], 1);
+      const int c = ncta + atomicAdd(plan.sched, 1);
       return c < plan.total_units ? c : plan.total_units;
     };
     for (int i = 0;; ++i, ++ucnt) {
       int unit = cta + i * ncta;
-      if (kDynSched) {
+      if (dyn) {
         // this role needs the next unit first: claim it and publish it to the others
         if (lane == 0) {
           unit = i == 0 ? cta : (nxt_claim >= 0 ? nxt_claim : claim());
@@ -1048,13 +1049,13 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
   }
 #endif
   if (warp == kMmaWarp) ptx::tmem_dealloc(tmem, 512);
-  if (kDynSched && threadIdx.x == 0) {
-    // the last CTA of the launch resets the counter for the next launch on this slot
-    // (every CTA's claims precede its increment: __syncthreads above + fence)
+  if (dyn && threadIdx.x == 0) {
+    // the last CTA of the launch resets the counters for the next launch on this
+    // workspace (every CTA's claims precede its increment: __syncthreads above + fence)
     __threadfence();
-    if (atomicAdd(&g_tc2_sched[plan.sched_slot][1], 1) == ncta - 1) {
-      atomicExch(&g_tc2_sched[plan.sched_slot][0], 0);
-      atomicExch(&g_tc2_sched[plan.sched_slot][1], 0);
+    if (atomicAdd(plan.sched + 1, 1) == ncta - 1) {
+      atomicExch(plan.sched, 0);
+      atomicExch(plan.sched + 1, 0);
     }
   }
 }
@@ -1084,14 +1085,13 @@ mixed_tc_kernel(const __grid_constant__ Plan rplan, const __grid_constant__ CUte
                 const __grid_constant__ Plan uplan, const __nv_bfloat16 *__restrict__ q_blk,
                 const __nv_bfloat16 *__restrict__ k_cache, const __nv_bfloat16 *__restrict__ v_cache,
                 const int32_t *__restrict__ idx, __nv_bfloat16 *__restrict__ out_blk, const int n_ref,
-                int32_t *__restrict__ sel_idx, float *__restrict__ ws_part, int32_t *__restrict__ ws_flags) {
+                int32_t *__restrict__ sel_idx) {
   if ((int)blockIdx.x < n_ref) {
     pdl_wait_then_trigger();
     refresh_tc2_body<128>(rplan, tm_q, tm_k, tm_v, tm_o, out, scores, sel_idx, (int)blockIdx.x, n_ref);
   } else {
     // (griddepcontrol.wait inside the body, after its input-independent prologue)
-    rtc::reuse_tc_body(uplan, q_blk, k_cache, v_cache, idx, out_blk, ws_part, ws_flags, (int)blockIdx.x - n_ref,
-                       (int)gridDim.x - n_ref);
+    rtc::reuse_tc_body(uplan, q_blk, k_cache, v_cache, idx, out_blk, (int)blockIdx.x - n_ref, (int)gridDim.x - n_ref);
   }
 }
 static_assert(THREADS == rtc::kTThreads, "mixed kernel: both bodies run 512-thread CTAs");
@@ -1106,13 +1106,6 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
       fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
   }
   return fn;
-}
-
-// launches in flight at the same time (different streams) get different counter
-// slots; a CUDA graph replays its captured slot, stream-ordered with itself
-int next_sched_slot() {
-  static std::atomic<unsigned> seq{0};
-  return (int)(seq.fetch_add(1u, std::memory_order_relaxed) % (unsigned)kSchedSlots);
 }
 
 int num_sms() {
@@ -1167,7 +1160,7 @@ cudaError_t make_maps(const Plan &plan, const void *q, const void *k, const void
 
 template <int D>
 cudaError_t launch_d(const Plan &plan, const void *q, const void *k, const void *v, void *out, float *scores,
-                     int32_t *sel_idx, cudaStream_t st) {
+                     int32_t *sel_idx, void *workspace, cudaStream_t st) {
   CUtensorMap tq, tk, tv, to;
   cudaError_t me = make_maps<D>(plan, q, k, v, out, tq, tk, tv, to);
   if (me != cudaSuccess) return me;
@@ -1176,9 +1169,9 @@ cudaError_t launch_d(const Plan &plan, const void *q, const void *k, const void 
   if (e != cudaSuccess) return e;
   const int grid = plan.total_units < num_sms() ? plan.total_units : num_sms();
   if (grid <= 0) return cudaSuccess;
-  static thread_local Plan pl;   // + the scheduler slot of this launch
+  static thread_local Plan pl;   // + this launch's scheduler counters
   pl = plan;
-  pl.sched_slot = next_sched_slot();
+  pl.sched = workspace_sched(workspace);
   return launch_pdl(refresh_tc2_kernel<D>, dim3(grid), dim3(THREADS), smem, st, pl, tq, tk, tv, to,
                     (__nv_bfloat16 *)out, scores, sel_idx);
 }
@@ -1198,13 +1191,11 @@ cudaError_t launch_mixed_tc(const Plan &rplan, const void *q, const void *k, con
   if (grid <= 0) return cudaSuccess;
   static thread_local Plan rpl;
   rpl = rplan;
-  rpl.sched_slot = next_sched_slot();
-  float *ws_part = nullptr;
-  int32_t *ws_flags = nullptr;
-  workspace_split(workspace, ws_part, ws_flags);
+  rpl.sched = workspace_sched(workspace);
+  (void)workspace;
   return launch_pdl(mixed_tc_kernel, dim3(grid), dim3(THREADS), smem, st, rpl, tq, tk, tv, to, (__nv_bfloat16 *)out,
                     scores, uplan, (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k, (const __nv_bfloat16 *)v,
-                    idx, (__nv_bfloat16 *)out_blk, n_ref, sel_idx, ws_part, ws_flags);
+                    idx, (__nv_bfloat16 *)out_blk, n_ref, sel_idx);
 }
 
 int num_sms_mixed() { return num_sms(); }
@@ -1219,10 +1210,10 @@ int refresh_tc2_units(int L, int bs, int be, int H, bool with_scores) {
 }
 
 cudaError_t launch_refresh_tc2(const Plan &plan, const void *q, const void *k, const void *v, void *out,
-                               float *scores, int32_t *sel_idx, cudaStream_t st) {
+                               float *scores, int32_t *sel_idx, void *workspace, cudaStream_t st) {
   switch (plan.D) {
-    case 64: return launch_d<64>(plan, q, k, v, out, scores, sel_idx, st);
-    case 128: return launch_d<128>(plan, q, k, v, out, scores, sel_idx, st);
+    case 64: return launch_d<64>(plan, q, k, v, out, scores, sel_idx, workspace, st);
+    case 128: return launch_d<128>(plan, q, k, v, out, scores, sel_idx, workspace, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -7,7 +7,6 @@
 #include <mutex>
 
 #include "reuse_tc_body.cuh"
-#include "workspace.h"
 
 #ifdef DLLM_TRACE
 extern "C" __attribute__((visibility("default"))) int dllm_trace_rtc_read(long long *cta, long long *chunk) {
@@ -25,10 +24,9 @@ using namespace rtc;
 __global__ void __launch_bounds__(kTThreads, 1)
 reuse_tc_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restrict__ q_blk,
                 const __nv_bfloat16 *__restrict__ k_cache, const __nv_bfloat16 *__restrict__ v_cache,
-                const int32_t *__restrict__ idx, __nv_bfloat16 *__restrict__ out, float *__restrict__ ws_part,
-                int32_t *__restrict__ ws_flags) {
+                const int32_t *__restrict__ idx, __nv_bfloat16 *__restrict__ out) {
   // (griddepcontrol.wait inside the body, after the input-independent prologue)
-  reuse_tc_body(plan, q_blk, k_cache, v_cache, idx, out, ws_part, ws_flags, (int)blockIdx.x, (int)gridDim.x);
+  reuse_tc_body(plan, q_blk, k_cache, v_cache, idx, out, (int)blockIdx.x, (int)gridDim.x);
 }
 
 int num_sms_tc() {
@@ -46,19 +44,14 @@ int num_sms_tc() {
 
 bool reuse_tc_supported(int D) { return D == kTD; }
 
-// CTAs for a Reuse plan: one per SM, fewer when the launch has too few keys to
-// give every CTA a few chunks
+// CTAs for a Reuse plan: one per SM (persistent), at most one per unit
 int reuse_tc_grid(const Plan &plan, int max_ctas) {
-  constexpr int64_t kMinCostPerCta = 4 * kTChunk;
-  if (plan.total_units <= 0) return 0;
-  int64_t g = (plan.total_cost + kMinCostPerCta - 1) / kMinCostPerCta;
-  if (g > max_ctas) g = max_ctas;
-  if (g > kMaxCtas) g = kMaxCtas;
-  return g < 1 ? 1 : (int)g;
+  return plan.total_units < max_ctas ? plan.total_units : max_ctas;
 }
 
 cudaError_t launch_reuse_tc(const Plan &plan, const void *q_blk, const void *k_cache, const void *v_cache,
                             const int32_t *idx, void *out, void *workspace, cudaStream_t st) {
+  (void)workspace;
   if (plan.D != kTD) return cudaErrorInvalidValue;
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
@@ -68,12 +61,9 @@ cudaError_t launch_reuse_tc(const Plan &plan, const void *q_blk, const void *k_c
   if (attr != cudaSuccess) return attr;
   const int grid = reuse_tc_grid(plan, num_sms_tc());
   if (grid <= 0) return cudaSuccess;
-  float *ws_part = nullptr;
-  int32_t *ws_flags = nullptr;
-  workspace_split(workspace, ws_part, ws_flags);
   return launch_pdl(reuse_tc_kernel, dim3(grid), dim3(kTThreads), (size_t)kTBytes, st, plan,
                     (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k_cache, (const __nv_bfloat16 *)v_cache, idx,
-                    (__nv_bfloat16 *)out, ws_part, ws_flags);
+                    (__nv_bfloat16 *)out);
 }
 
 }  // namespace dllm

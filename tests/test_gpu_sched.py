@@ -1,8 +1,10 @@
-"""GPU: the dynamic unit schedulers of the tcgen05 Refresh and Reuse kernels
-(device claim counters in 64 self-resetting per-launch slots).
+"""GPU: the dynamic unit scheduler of the tcgen05 Refresh kernel (device claim
+counters in the caller's workspace, dllm_problem.workspace).
 Which CTA computes which work unit must not change any result: repeated
-launches (wrapping the slots), launches on two streams in flight at once and
-CUDA-graph replays are all bit-identical to one reference launch."""
+launches (the counters self-reset), launches of two problems (two workspaces)
+on two streams in flight at once, CUDA-graph replays and the static schedule
+without a workspace are all bit-identical to one reference launch, and every
+launch leaves the workspace zeroed."""
 import pytest
 import torch
 
@@ -41,14 +43,38 @@ def _same(a, b):
     assert torch.equal(a.out_blk.view(torch.int16), b.out_blk.view(torch.int16))
 
 
-def test_repeated_launches_wrap_the_counter_slots(L):
+def test_repeated_launches_reset_the_counters(L):
     args = _setup(L, "C3", 12)
     ref = _run(L, *args)
     torch.cuda.synchronize()
-    for _ in range(70):          # > 64 slots: every slot reused after its reset
+    for _ in range(20):
         got = _run(L, *args)
     torch.cuda.synchronize()
     _same(ref, got)
+    assert int(args[0].workspace.count_nonzero()) == 0, "the launches must leave the workspace zeroed"
+
+
+def test_static_schedule_without_workspace(L):
+    p, q, q_blk, kc, vc = _setup(L, "C2", 4)
+    ref = _run(L, p, q, q_blk, kc, vc)
+    wl = synth.config("C2", num_requests=4)
+    p0 = L.Problem(wl.seq_len, wl.blk_start, wl.blk_end, num_heads=wl.num_heads, num_kv_heads=wl.num_kv_heads,
+                   head_dim=wl.head_dim, keep_ratio=wl.keep_ratio, pool_window=wl.pool_window,
+                   page_size=wl.page_size, block_table=p.block_table, workspace=None)
+    got = _run(L, p0, q, q_blk, kc, vc)
+    torch.cuda.synchronize()
+    _same(ref, got)
+
+
+def test_workspace_validation(L):
+    p, q, q_blk, kc, vc = _setup(L, "C0", None)
+    wl = synth.config("C0")
+    small = torch.zeros(L.workspace_bytes() - 16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(L.DllmError):
+        bad = L.Problem(wl.seq_len, wl.blk_start, wl.blk_end, num_heads=wl.num_heads, num_kv_heads=wl.num_kv_heads,
+                        head_dim=wl.head_dim, keep_ratio=wl.keep_ratio, pool_window=wl.pool_window,
+                        page_size=wl.page_size, block_table=p.block_table, workspace=small)
+        _run(L, bad, q, q_blk, kc, vc)
 
 
 def test_two_streams_in_flight(L):
