@@ -1,31 +1,42 @@
 #!/usr/bin/env python
 """Benchmark of the Head-Centric Sparse Attention hot path (one JSON line).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1] [--scaling weak|strong]
+                    [--impl ours|reference] [--no-configs]
     torchrun --nproc-per-node N bench.py --gpus N ...     (one process per GPU, NCCL)
 
 A step = one pass of the whole hot path over one batch:
 dllm_refresh_attn (Eq. 3 + importance) -> dllm_select_heads (Eq. 6 + TopK) ->
-dllm_reuse_sparse_attn (Eq. 4), through the C-ABI.  At N=1 the batch is
-BASELINE.json configs[1] (C1, LLaDA-8B layer shape: 16 requests, 32 heads,
-D=128, L=1024, block 32, keep 0.25).  At N>1 every rank runs its LPT shard of
-an N-times-replicated batch (weak scaling: 16 requests per GPU); there is no
-collective on the data path (requests are independent).  The NCCL all-gather
-of the per-request outputs is timed separately (`allgather_ms`).
+dllm_reuse_sparse_attn (Eq. 4), through the C-ABI; for the mixed burst batch
+(C3) the Refresh requests run Refresh + select and the others Reuse, in one
+launch (dllm_mixed_attn) + the select.  `value` is measured on --config (default
+C1, BASELINE.json configs[1], LLaDA-8B layer shape on 1 B200).
+
+Multi-GPU: requests are independent, so the batch is LPT-partitioned over the
+ranks with no collective on the data path.  --scaling weak (default): every rank
+holds a C-sized shard of an N-times replicated batch; --scaling strong: the
+config's own batch is partitioned (C3: 256 requests over 8 GPUs = 32 each).  The
+NCCL all-gather of the per-request outputs (Refresh rows, new index lists,
+Reuse rows) is timed separately: serial, and overlapped with the next step's
+compute on a side stream.
 
 value  = requests/s over all ranks = (requests per step * K) / max-over-ranks
-         device time of the K steps (CUDA events on the launch stream; L2
-         flushed before every step by a 512 MiB write outside the events).
+         device time of the K steps (CUDA graph replay of the step; CUDA events on
+         the launch stream; L2 flushed before every step by a 512 MiB write
+         outside the events).
+kernels = per-kernel CUDA-event times of eager launches (one kernel between two
+         events, L2 flushed before each), against the measured peaks; Reuse also
+         "in stream": a CUDA graph of 31 back-to-back Reuse launches (the Reuse
+         steps of one block cycle) rotating over 3 input sets so
+         that no launch finds its K/V in L2, per-launch time = graph time / 31.
+configs = the same sub-results for the other BASELINE configs (N=1 only):
+         C2 (Dream GQA), C3 (burst mix), C4 (r = 0.25), and the N4 LM head.
 e2e    = the same metric through the public API with HOST buffers: every step
-         copies its inputs from pinned host memory to the device, runs the
-         three calls and copies the results back (all inside the events).
-roofline = the dominant kernel (Refresh, tensor-bound) against the measured
-         bf16 peak in MEASURED_PEAKS.json; Reuse / select are reported in
-         `kernels` against the measured HBM copy bandwidth.
+         copies its inputs from pinned host memory to the device, runs the calls
+         and copies the results back (pipelined as a serving loop would).
 cpu_baseline = the fp64 oracle (oracle/) timed on this host's cores on a
          bounded sample of the same workload (rank 0, N=1 only).
---impl reference runs that oracle as the reference arm (BASELINE has no
-         runnable reference implementation: the paper ships no code).
+--impl reference runs that oracle as the reference arm (the paper ships no code).
 """
 from __future__ import annotations
 
@@ -44,6 +55,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Reuse sparse-attn HBM GB/s and Refresh TFLOPS vs peak; requests/s at 1/2/4/8 B200"
 UNIT = "requests/s"
+BLOCK_CYCLE_REUSE = 31   # Reuse steps per Refresh (gen 256 / steps 256 / block 32)
 
 
 def load_peaks():
@@ -55,10 +67,11 @@ def load_peaks():
         return 1590.0, 1400.0, 6650.0, "fallback"
 
 
-def workload_desc(wl, n):
+def workload_desc(wl, n, scaling):
     mix = "" if wl.refresh_mask is None else \
-        f" ({sum(wl.refresh_mask)} Refresh+select+Reuse, {wl.num_requests - sum(wl.refresh_mask)} Reuse-only)"
-    return (f"{wl.name}: {wl.num_requests} requests/GPU{mix} x {n} GPU, H={wl.num_heads}, H_kv={wl.num_kv_heads}, "
+        f" ({sum(wl.refresh_mask)} Refresh+select, {wl.num_requests - sum(wl.refresh_mask)} Reuse-only)"
+    per = "requests/GPU" if scaling == "weak" else "requests in total"
+    return (f"{wl.name}: {wl.num_requests} {per}{mix} x {n} GPU, H={wl.num_heads}, H_kv={wl.num_kv_heads}, "
             f"D={wl.head_dim}, L={min(wl.seq_len)}..{max(wl.seq_len)}, blk={wl.blk[0]}, r={wl.keep_ratio}, "
             f"w={wl.pool_window}, page={wl.page_size}")
 
@@ -66,10 +79,9 @@ def workload_desc(wl, n):
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     """SM clocks, power and throttle reasons sampled through NVML every ~2 ms while
-    the timed region runs (samples taken before the region starts are dropped).
-    The timed region of a default run is only a few ms, so `extend(fn, seconds)`
-    keeps replaying the same step afterwards, untimed, and records the clocks the
-    workload settles at under the power cap (reported separately)."""
+    the timed region runs.  The timed region of a default run is short, so
+    `extend(fn, seconds)` keeps replaying the same step afterwards, untimed, and
+    records the clocks the workload settles at under the power cap (separately)."""
 
     def __init__(self, index: int):
         self.index, self.samples, self._stop = index, [], threading.Event()
@@ -113,8 +125,6 @@ class ClockSampler:
         self._phase = None
 
     def extend(self, fn, seconds: float = 0.2):
-        """Replay `fn` (one untimed step, device-synchronised by the caller's loop)
-        for about `seconds` with sampling on, then stop the sampler."""
         import torch
         self._phase = "extended"
         t0 = time.perf_counter()
@@ -148,11 +158,12 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) timing
-def cpu_oracle_rate(wl, budget_s: float = 12.0, max_requests: int | None = None):
-    """The fp64 oracle as it stands, on a bounded sample of the workload's
-    requests (whole requests: Refresh + importance + select + Reuse, all heads;
-    in a mixed batch the Refresh requests run Refresh + select and the
-    reuse-only requests run Reuse alone on the same index lists as the GPU arm).  Returns (requests/s, requests timed, seconds, threads).
+def cpu_oracle_rate(wl, budget_s: float = 12.0, max_requests: int | None = None, time_inputs: bool = False):
+    """The fp64 oracle as it stands, on a bounded sample of the workload's requests
+    (whole requests: Refresh + importance + select + Reuse, all heads; in a mixed
+    batch the Refresh requests run Refresh + select and the Reuse-only requests
+    Reuse on generated index lists).  Input generation is outside the timed region
+    unless time_inputs.  Returns (requests/s, requests timed, seconds, threads).
     For a mixed batch the rate is the batch's request count over the batch time
     extrapolated from the per-kind mean request times of the sample."""
     import torch
@@ -168,13 +179,12 @@ def cpu_oracle_rate(wl, budget_s: float = 12.0, max_requests: int | None = None)
     done, t_total = 0, 0.0
     for kd, reqs in zip(kinds, order):
         t_kind, n_kind = 0.0, 0
-        # whole passes over the requests until the time budget is spent (C1 has only
-        # 16 requests: a single pass is ~3 s of oracle time)
         for b in (reqs * 8 if max_requests is None else reqs):
             if max_requests is not None and done >= max_requests:
                 break
             q, K, V, qb = (t.double().numpy() for t in synth.request_tensors(wl, b))
             bs, be, L = wl.blk_start[b], wl.blk_end[b], wl.seq_len[b]
+            sel = None
             if not kd:
                 k = O.keep_count(wl.keep_ratio, L - (be - bs))
                 sel = synth.indices(synth.subset(wl, [b]), [k])[0]
@@ -184,7 +194,6 @@ def cpu_oracle_rate(wl, budget_s: float = 12.0, max_requests: int | None = None)
                 raw = O.raw_scores(q[bs:be], K)
                 sel = O.select_batch([raw], [L], [bs], [be], wl.keep_ratio, wl.pool_window)[0]
             if not kd or wl.refresh_mask is None:
-                # mixed (C3) batches: Refresh requests stop at select, as on the GPU leg
                 O.attention_with_cache(qb, K, V, bs, be, sel)
             dt = time.perf_counter() - t0
             t_kind += dt
@@ -201,7 +210,6 @@ def cpu_oracle_rate(wl, budget_s: float = 12.0, max_requests: int | None = None)
     return wl.num_requests / t_batch, done, t_total, cores
 
 
-# ----------------------------------------------------------------------------- ncu traffic
 def ncu_traffic(kernel: str, cfg: str):
     """dram read+write bytes per launch from the committed `ncu --set full`
     summary (profiles/ncu_traffic.json), or None."""
@@ -221,25 +229,336 @@ def run_reference(args):
         return
     from paper_2512_17077_b200 import synth
     wl = synth.config(args.config)
-    rates = []
     for _ in range(args.warmup):
         cpu_oracle_rate(wl, budget_s=0.0, max_requests=1)
-    t0 = time.perf_counter()
-    n_req = 0
+    n_req, t_oracle = 0, 0.0
     for _ in range(args.steps):
+        # the oracle alone is timed (inputs are generated outside the measured region)
         r, n, t, cores = cpu_oracle_rate(wl, budget_s=0.0, max_requests=1)
-        rates.append(r)
         n_req += n
-    wall = time.perf_counter() - t0
-    value = n_req / wall
+        t_oracle += t
+    value = n_req / t_oracle
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_desc(wl, 1), "sample": "1 request (all heads) per step"},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_oracle / args.steps,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": workload_desc(wl, 1, args.scaling), "sample": "1 request (all heads) per step"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
-                             "sample": f"{args.steps} steps x 1 request of {wl.name} (Refresh+select+Reuse, all heads)"},
+                             "sample": f"{args.steps} steps x 1 request of {wl.name} (Refresh+select+Reuse, all "
+                                       "heads; oracle time only, input generation excluded)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- one config on this rank
+class Step:
+    """The batch of this rank (an LPT shard of `glob`), its problems / buffers and
+    the step closure."""
+
+    def __init__(self, glob, parts, rank, dev, lib, synth):
+        import torch
+        self.torch, self.lib, self.synth, self.dev = torch, lib, synth, dev
+        self.glob, self.parts, self.rank = glob, parts, rank
+        wl = synth.subset(glob, parts[rank])
+        self.wl = wl
+        self.pieces = []
+        if wl.refresh_mask is None:
+            self.pieces = [self._make_piece(wl, True, True)]
+        else:
+            ri = [i for i, m in enumerate(wl.refresh_mask) if m]
+            ui = [i for i, m in enumerate(wl.refresh_mask) if not m]
+            shared = synth.make_batch(wl)
+            dk, dv = shared.k_cache.to(dev), shared.v_cache.to(dev)
+            if ri:
+                self.pieces.append(self._make_shared(shared, dk, dv, ri, True))
+            if ui:
+                self.pieces.append(self._make_shared(shared, dk, dv, ui, False))
+        # both phases of a mixed batch in ONE launch (dllm_mixed_attn, next row N3)
+        self.mixed = len(self.pieces) == 2
+
+    def _problem(self, sub, block_table):
+        return self.lib.Problem(sub.seq_len, sub.blk_start, sub.blk_end, num_heads=sub.num_heads,
+                                num_kv_heads=sub.num_kv_heads, head_dim=sub.head_dim, keep_ratio=sub.keep_ratio,
+                                pool_window=sub.pool_window, page_size=sub.page_size,
+                                block_table=block_table.contiguous().to(self.dev))
+
+    def _prefill_idx(self, sub, pp, bf):
+        # Reuse-only requests bring the index lists of an earlier selection
+        kk = pp.layout()[0]
+        flat = np.concatenate([x.reshape(-1) for x in self.synth.indices(sub, kk)]).astype(np.int32)
+        if flat.size:
+            bf.idx[:flat.size].copy_(self.torch.from_numpy(flat))
+
+    def _make_piece(self, sub, refresh, reuse):
+        bt = self.synth.make_batch(sub)
+        pp = self._problem(sub, bt.block_table)
+        tens = [t.to(self.dev) for t in (bt.q, bt.q_blk, bt.k_cache, bt.v_cache)]
+        bf = self.lib.alloc_buffers(pp, device=self.dev)
+        if not refresh:
+            self._prefill_idx(sub, pp, bf)
+        host = {"q": bt.q, "q_blk": bt.q_blk, "k_cache": bt.k_cache, "v_cache": bt.v_cache}
+        return {"wl": sub, "p": pp, "t": tens, "buf": bf, "refresh": refresh, "reuse": reuse, "host": host}
+
+    def _make_shared(self, shared, dk, dv, reqs, refresh):
+        # a phase of a mixed batch: its own problem (block-table rows of its requests)
+        # over the batch's ONE paged cache
+        sub = self.synth.subset(self.wl, reqs)
+        pp = self._problem(sub, shared.block_table[reqs])
+        q = self.torch.cat([shared.q_req(b) for b in reqs])
+        qb = self.torch.cat([shared.q_blk_req(b) for b in reqs])
+        bf = self.lib.alloc_buffers(pp, device=self.dev)
+        if not refresh:
+            self._prefill_idx(sub, pp, bf)
+        host = {"q": q, "q_blk": qb, "k_cache": shared.k_cache, "v_cache": shared.v_cache}
+        return {"wl": sub, "p": pp, "t": [q.to(self.dev), qb.to(self.dev), dk, dv], "buf": bf, "refresh": refresh,
+                "reuse": not refresh, "host": host}
+
+    def step(self, ev=None, bufs=None):
+        """One step on the current stream; ev = 4 events around Refresh / select /
+        Reuse (or the mixed launch / select); bufs overrides the output buffers."""
+        lib = self.lib
+        stream = self.torch.cuda.current_stream(self.dev)
+        bufs = bufs or [pc["buf"] for pc in self.pieces]
+        rec = (lambda i: ev[i].record(stream)) if ev is not None else (lambda i: None)
+        if self.mixed:
+            (pr, pu), (br, bu) = self.pieces, bufs
+            q, _, kc, vc = pr["t"]
+            rec(0)
+            lib.mixed_attn(pr["p"], q, br.out, br.scores, pu["p"], pu["t"][1], bu.idx, bu.out_blk, kc, vc, stream)
+            rec(1)
+            lib.select_heads(pr["p"], br.scores, br.idx, stream)
+            rec(2)
+            rec(3)
+            return
+        rec(0)
+        for pc, bf in zip(self.pieces, bufs):
+            if pc["refresh"]:
+                q, qb, kc, vc = pc["t"]
+                lib.refresh_attn(pc["p"], q, kc, vc, bf.out, bf.scores, stream)
+        rec(1)
+        for pc, bf in zip(self.pieces, bufs):
+            if pc["refresh"]:
+                lib.select_heads(pc["p"], bf.scores, bf.idx, stream)
+        rec(2)
+        for pc, bf in zip(self.pieces, bufs):
+            if pc["reuse"]:
+                q, qb, kc, vc = pc["t"]
+                lib.reuse_sparse_attn(pc["p"], qb, kc, vc, bf.idx, bf.out_blk, stream)
+        rec(3)
+
+    def algorithmic(self):
+        """Refresh FLOPs, Reuse unique / logical bytes and select bytes of one step
+        (DESIGN.md §6); unique rows are counted from the index lists in use."""
+        flops = 0.0
+        reuse_u = reuse_l = sel = 0
+        for pc in self.pieces:
+            sub = pc["wl"]
+            H, Hk, D = sub.num_heads, sub.num_kv_heads, sub.head_dim
+            g = H // Hk
+            kk, total_idx, rows, blk_rows = pc["p"].layout()
+            idx_host = pc["buf"].idx[:total_idx].cpu().numpy()
+            uniq, off = 0, 0
+            for b in range(sub.num_requests):
+                rb = idx_host[off:off + H * kk[b]].reshape(H, kk[b])
+                off += H * kk[b]
+                for kv in range(Hk):
+                    uniq += len(np.unique(rb[kv * g:(kv + 1) * g])) + sub.blk[b]
+            if pc["reuse"]:
+                extra = 2 * blk_rows * H * D * 2 + 4 * total_idx
+                reuse_u += uniq * 2 * D * 2 + extra
+                reuse_l += sum(H * (sub.blk[b] + kk[b]) for b in range(sub.num_requests)) * 2 * D * 2 + extra
+            if pc["refresh"]:
+                flops += sum(4.0 * H * L * L * D for L in sub.seq_len)
+                sel += 4 * H * rows + 4 * total_idx
+        return flops, reuse_u, reuse_l, sel
+
+
+def time_eager(st, steps, warmup, flush):
+    """Per-kernel CUDA-event times (s) of eager steps, L2 flushed before each."""
+    torch = st.torch
+    for _ in range(warmup):
+        flush.zero_()
+        st.step()
+    torch.cuda.synchronize(st.dev)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    for i in range(steps):
+        flush.zero_()
+        st.step(evs[i])
+    torch.cuda.synchronize(st.dev)
+    el = lambda i, a, b: evs[i][a].elapsed_time(evs[i][b]) * 1e-3  # noqa: E731
+    return ([el(i, 0, 1) for i in range(steps)], [el(i, 1, 2) for i in range(steps)],
+            [el(i, 2, 3) for i in range(steps)], [el(i, 0, 3) for i in range(steps)])
+
+
+def capture_graph(st):
+    torch = st.torch
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream(st.dev)
+    cs.wait_stream(torch.cuda.current_stream(st.dev))
+    with torch.cuda.stream(cs):
+        st.step()   # warm the capture stream
+    torch.cuda.current_stream(st.dev).wait_stream(cs)
+    torch.cuda.synchronize(st.dev)
+    with torch.cuda.graph(g, stream=cs):
+        st.step()
+    return g
+
+
+def time_graph(st, g, steps, warmup, flush, clk=None, dist=None):
+    torch = st.torch
+    stream = torch.cuda.current_stream(st.dev)
+    for _ in range(warmup):
+        flush.zero_()
+        g.replay()
+    torch.cuda.synchronize(st.dev)
+    gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(st.dev)
+    if clk is not None:
+        clk.__enter__()
+    for i in range(steps):
+        flush.zero_()
+        gev[i][0].record(stream)
+        g.replay()
+        gev[i][1].record(stream)
+    torch.cuda.synchronize(st.dev)
+    if clk is not None:
+        clk.__exit__()
+        clk.extend(g.replay, 0.25)
+    if dist is not None:
+        dist.barrier()
+    return sum(gev[i][0].elapsed_time(gev[i][1]) * 1e-3 for i in range(steps))
+
+
+def reuse_in_stream(st, reps=BLOCK_CYCLE_REUSE, iters=5):
+    """Reuse per-launch time in a stream of back-to-back launches: one CUDA graph of
+    `reps` launches rotating over independent input sets (3 when the step's unique
+    Reuse bytes are below 4x L2, else the step's own set), so launch latency
+    overlaps the previous launch (PDL) but no launch finds its rows in L2."""
+    import torch
+    lib, synth, dev = st.lib, st.synth, st.dev
+    pc = st.pieces[0]
+    sets = [(pc["p"], pc["t"][1], pc["t"][2], pc["t"][3], pc["buf"])]
+    base = st.wl
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    nsets = 3 if st.algorithmic()[1] < 4 * l2 else 1
+    for s in range(1, nsets):
+        wl = synth.replicate(base, nsets)   # replica s: the same shapes, its own values
+        sub = synth.subset(wl, list(range(s * base.num_requests, (s + 1) * base.num_requests)))
+        bt = synth.make_batch(sub)
+        pp = lib.Problem(sub.seq_len, sub.blk_start, sub.blk_end, num_heads=sub.num_heads,
+                         num_kv_heads=sub.num_kv_heads, head_dim=sub.head_dim, keep_ratio=sub.keep_ratio,
+                         pool_window=sub.pool_window, page_size=sub.page_size, block_table=bt.block_table.to(dev))
+        bf = lib.alloc_buffers(pp, device=dev)
+        kk = pp.layout()[0]
+        flat = np.concatenate([x.reshape(-1) for x in synth.indices(sub, kk)]).astype(np.int32)
+        bf.idx[:flat.size].copy_(torch.from_numpy(flat))
+        sets.append((pp, bt.q_blk.to(dev), bt.k_cache.to(dev), bt.v_cache.to(dev), bf))
+    cs = torch.cuda.Stream(dev)
+
+    def launches():
+        for i in range(reps):
+            pp, qb, kc, vc, bf = sets[i % nsets]
+            lib.reuse_sparse_attn(pp, qb, kc, vc, bf.idx, bf.out_blk, cs)
+
+    cs.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(cs):
+        launches()
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cs):
+        launches()
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    ts = []
+    stream = torch.cuda.current_stream(dev)
+    for it in range(iters + 2):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if it >= 2:
+            ts.append(e0.elapsed_time(e1) * 1e-3 / reps)
+    return statistics.median(ts)
+
+
+def lm_head_result(dev, lib, synth, tf_peak, iters=10):
+    """N4: dllm_lm_head_argmax at the LLaDA-8B LM head (2,048 x 4,096 x 126,464)."""
+    import torch
+    f = synth.LM_HEAD_FULL
+    n, d, v = f["n_tok"], f["d_model"], f["vocab"]
+    h, w = synth.lm_head_inputs(n, d, v, "realistic")
+    h, w = h.to(dev), w.to(dev)
+    ids = torch.empty(n, dtype=torch.int32, device=dev)
+    ws = torch.empty(lib.lm_head_workspace_bytes(n, v, f["max_num_logits"]), dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        lib.lm_head_argmax(h, w, ids, f["max_num_logits"], ws)
+    torch.cuda.synchronize(dev)
+    ts = []
+    for _ in range(iters):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        lib.lm_head_argmax(h, w, ids, f["max_num_logits"], ws)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ts.append(e0.elapsed_time(e1) * 1e-3)
+    t = statistics.median(ts)
+    flop = 2.0 * n * d * v
+    return {"kernel": "dllm_lm_head_argmax (tcgen05 GEMM + fused argmax)", "shape": [n, d, v],
+            "max_num_logits": f["max_num_logits"], "us": t * 1e6, "TFLOP/s": flop / t / 1e12,
+            "frac": flop / t / 1e12 / tf_peak, "bound": "tensor", "weight_bytes": v * d * 2,
+            "note": "weight (1.04 GB) larger than L2: no flush needed"}
+
+
+def kernels_result(st, t_ref, t_sel, t_reu, tf_peak, hbm_peak, reuse_stream_s=None):
+    flops, reuse_u, reuse_l, sel = st.algorithmic()
+    m = statistics.mean
+    if st.mixed:
+        t_roof = flops / (tf_peak * 1e12) + reuse_u / (hbm_peak * 1e9)
+        return {
+            "mixed": {"us": 1e6 * m(t_ref), "refresh_flop": flops, "reuse_bytes_unique": reuse_u,
+                      "reuse_bytes_logical": reuse_l, "roofline_us": 1e6 * t_roof, "frac": t_roof / m(t_ref),
+                      "frac_definition": "additive roofline time (Refresh FLOP / bf16 peak + Reuse unique bytes / "
+                                         "HBM peak) / measured launch time"},
+            "select": {"us": 1e6 * m(t_sel), "GB/s": sel / m(t_sel) / 1e9, "frac": sel / m(t_sel) / 1e9 / hbm_peak,
+                       "bytes_per_launch": sel},
+        }, flops, reuse_u
+    a_ref = flops / m(t_ref) / 1e12
+    out = {
+        "refresh": {"us": 1e6 * m(t_ref), "TFLOP/s": a_ref, "frac": a_ref / tf_peak, "flop_per_launch": flops,
+                    "bound": "tensor", "peak": tf_peak},
+        "select": {"us": 1e6 * m(t_sel), "GB/s": sel / m(t_sel) / 1e9, "frac": sel / m(t_sel) / 1e9 / hbm_peak,
+                   "bytes_per_launch": sel, "bound": "hbm (latency at these sizes)"},
+        "reuse": {"us": 1e6 * m(t_reu), "GB/s": reuse_u / m(t_reu) / 1e9, "frac": reuse_u / m(t_reu) / 1e9 / hbm_peak,
+                  "bytes_per_launch_unique": reuse_u, "bytes_per_launch_logical": reuse_l,
+                  "GB/s_logical": reuse_l / m(t_reu) / 1e9, "bound": "hbm", "peak": hbm_peak,
+                  "timing": "one launch between two CUDA events, L2 flushed before it"},
+        "block_cycle_us": 1e6 * (m(t_ref) + m(t_sel) + BLOCK_CYCLE_REUSE * m(t_reu)),
+    }
+    if reuse_stream_s is not None:
+        out["reuse"].update({
+            "us_in_stream": 1e6 * reuse_stream_s, "GB/s_in_stream": reuse_u / reuse_stream_s / 1e9,
+            "frac_in_stream": reuse_u / reuse_stream_s / 1e9 / hbm_peak,
+            "in_stream_timing": f"CUDA graph of {BLOCK_CYCLE_REUSE} back-to-back launches over 3 rotating input "
+                                "sets (no L2 reuse), graph time / launches"})
+        out["block_cycle_us_in_stream"] = 1e6 * (m(t_ref) + m(t_sel) + BLOCK_CYCLE_REUSE * reuse_stream_s)
+    return out, flops, reuse_u
+
+
+def config_result(cfg_name, dev, lib, synth, shard, tf_peak, hbm_peak, steps, warmup, flush):
+    """A sub-result for `configs`: one GPU, the whole config batch."""
+    wl = synth.config(cfg_name)
+    st = Step(wl, [list(range(wl.num_requests))], 0, dev, lib, synth)
+    t_ref, t_sel, t_reu, t_step = time_eager(st, steps, warmup, flush)
+    g = capture_graph(st)
+    total = time_graph(st, g, steps, warmup, flush)
+    rs = None if st.mixed else reuse_in_stream(st)
+    kern, flops, reuse_u = kernels_result(st, t_ref, t_sel, t_reu, tf_peak, hbm_peak, rs)
+    del g
+    return {"workload": workload_desc(wl, 1, "weak"), "requests_per_s": wl.num_requests * steps / total,
+            "ms_per_step": 1e3 * total / steps, "launch_mode": "cuda_graph", "kernels": kern}
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -249,15 +568,12 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C1")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C2/C3/C4/N4 sub-results (N=1 only anyway)")
+    ap.add_argument("--config-steps", type=int, default=5)
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph replay")
-    ap.add_argument("--no-mixed", action="store_true",
-                    help="C3: separate Refresh and Reuse launches instead of one mixed launch")
-    ap.add_argument("--fused-select", action="store_true",
-                    help="dllm_refresh_select_attn (select fused into the Refresh kernel when the library is built "
-                         "with DLLM_TC2_FUSEDSEL=1) instead of dllm_refresh_attn + dllm_select_heads")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -271,279 +587,264 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("DLLM_BENCH_BACKEND", "nccl")   # gloo: dev check of the multi-rank logic on 1 GPU
     if world > 1:
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    dev = torch.device("cuda", local_rank)
+        torch.cuda.set_device(local_rank if backend == "nccl" else 0)
+        dist.init_process_group(backend, **({"device_id": torch.device("cuda", local_rank)}
+                                            if backend == "nccl" else {}))
+    dev = torch.device("cuda", local_rank if backend == "nccl" else 0)
     torch.cuda.set_device(dev)
     tf_peak, tf_sust, hbm_peak, peak_src = load_peaks()
 
     base = synth.config(args.config)
-    glob = synth.replicate(base, world)
+    glob = synth.replicate(base, world) if args.scaling == "weak" else base
     k_glob = [lib.keep_count(glob.keep_ratio, L - (e - s)) for L, s, e in zip(glob.seq_len, glob.blk_start, glob.blk_end)]
-    costs = [shard.request_cost(L, e - s, glob.num_heads, glob.num_kv_heads, glob.head_dim, k)
-             for L, s, e, k in zip(glob.seq_len, glob.blk_start, glob.blk_end, k_glob)]
+    costs = shard.workload_costs(glob, k_glob)
     parts = shard.lpt_partition(costs, world)
-    wl = synth.subset(glob, parts[rank])
+    st = Step(glob, parts, rank, dev, lib, synth)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
-    # A step runs Refresh -> select -> Reuse for every request (C1/C2/C4: the whole
-    # hot path over the batch), except in a mixed (burst) batch (C3: refresh_mask,
-    # SURVEY §8(d)): there the Refresh requests run Refresh + select (their block
-    # output is the dense one; the new index lists serve their next Reuse steps)
-    # and the others run Reuse alone with the index lists of an earlier selection
-    # (generated once, outside the timed region).
-    def make_part(sub, refresh):
-        bt = synth.make_batch(sub)
-        pp = lib.Problem(sub.seq_len, sub.blk_start, sub.blk_end, num_heads=sub.num_heads,
-                         num_kv_heads=sub.num_kv_heads, head_dim=sub.head_dim, keep_ratio=sub.keep_ratio,
-                         pool_window=sub.pool_window, page_size=sub.page_size, block_table=bt.block_table.to(dev))
-        tens = [t.to(dev) for t in (bt.q, bt.q_blk, bt.k_cache, bt.v_cache)]
-        bf = lib.alloc_buffers(pp, device=dev)
-        if not refresh:
-            kk = pp.layout()[0]
-            flat = np.concatenate([x.reshape(-1) for x in synth.indices(sub, kk)]).astype(np.int32)
-            if flat.size:
-                bf.idx[:flat.size].copy_(torch.from_numpy(flat))
-        return {"wl": sub, "batch": bt, "p": pp, "t": tens, "buf": bf, "refresh": refresh, "reuse": True}
-
-    def make_part_shared(shared, dk, dv, reqs, refresh):
-        # a phase of a mixed batch: its own problem (block-table rows of its requests)
-        # over the batch's ONE paged cache
-        sub = synth.subset(wl, reqs)
-        pp = lib.Problem(sub.seq_len, sub.blk_start, sub.blk_end, num_heads=sub.num_heads,
-                         num_kv_heads=sub.num_kv_heads, head_dim=sub.head_dim, keep_ratio=sub.keep_ratio,
-                         pool_window=sub.pool_window, page_size=sub.page_size,
-                         block_table=shared.block_table[reqs].contiguous().to(dev))
-        q = torch.cat([shared.q_req(b) for b in reqs])
-        qb = torch.cat([shared.q_blk_req(b) for b in reqs])
-        bf = lib.alloc_buffers(pp, device=dev)
-        if not refresh:
-            kk = pp.layout()[0]
-            flat = np.concatenate([x.reshape(-1) for x in synth.indices(sub, kk)]).astype(np.int32)
-            if flat.size:
-                bf.idx[:flat.size].copy_(torch.from_numpy(flat))
-        host = {"q": q, "q_blk": qb, "k_cache": shared.k_cache, "v_cache": shared.v_cache}
-        return {"wl": sub, "host": host, "p": pp, "t": [q.to(dev), qb.to(dev), dk, dv], "buf": bf,
-                "refresh": refresh, "reuse": not refresh}
-
-    mixed = False
-    if wl.refresh_mask is None:
-        parts_local = [make_part(wl, True)]
-    else:
-        ri = [i for i, m in enumerate(wl.refresh_mask) if m]
-        ui = [i for i, m in enumerate(wl.refresh_mask) if not m]
-        shared = synth.make_batch(wl)
-        dk, dv = shared.k_cache.to(dev), shared.v_cache.to(dev)
-        parts_local = ([make_part_shared(shared, dk, dv, ri, True)] if ri else []) + \
-                      ([make_part_shared(shared, dk, dv, ui, False)] if ui else [])
-        # both phases in ONE launch (dllm_mixed_attn, next row N3) unless disabled
-        mixed = len(parts_local) == 2 and not args.no_mixed
-    for pt in parts_local:
-        if "host" not in pt:
-            bt = pt["batch"]
-            pt["host"] = {"q": bt.q, "q_blk": bt.q_blk, "k_cache": bt.k_cache, "v_cache": bt.v_cache}
-
-    fused = args.fused_select   # dllm_refresh_select_attn (one call; fused only in a DLLM_TC2_FUSEDSEL=1 build)
-    fused_in_kernel = fused and "select_in_refresh=on" in lib.version()
-
-    def step(ev=None):
-        stream = torch.cuda.current_stream(dev)   # the capture stream while a graph is recorded
-        if mixed:
-            pr, pu = parts_local
-            q, _, kc, vc = pr["t"]
-            qb = pu["t"][1]
-            if ev is not None:
-                ev[0].record(stream)
-            if fused:
-                lib.mixed_select_attn(pr["p"], q, pr["buf"].out, pr["buf"].scores, pr["buf"].idx, pu["p"], qb,
-                                      pu["buf"].idx, pu["buf"].out_blk, kc, vc, stream)
-            else:
-                lib.mixed_attn(pr["p"], q, pr["buf"].out, pr["buf"].scores, pu["p"], qb, pu["buf"].idx,
-                               pu["buf"].out_blk, kc, vc, stream)
-            if ev is not None:
-                ev[1].record(stream)
-            if not fused:
-                lib.select_heads(pr["p"], pr["buf"].scores, pr["buf"].idx, stream)
-            if ev is not None:
-                ev[2].record(stream)
-                ev[3].record(stream)
-            return
-        if ev is not None:
-            ev[0].record(stream)
-        for pt in parts_local:
-            if pt["refresh"]:
-                q, qb, kc, vc = pt["t"]
-                if fused:
-                    lib.refresh_select_attn(pt["p"], q, kc, vc, pt["buf"].out, pt["buf"].scores, pt["buf"].idx, stream)
-                else:
-                    lib.refresh_attn(pt["p"], q, kc, vc, pt["buf"].out, pt["buf"].scores, stream)
-        if ev is not None:
-            ev[1].record(stream)
-        for pt in parts_local:
-            if pt["refresh"] and not fused:
-                lib.select_heads(pt["p"], pt["buf"].scores, pt["buf"].idx, stream)
-        if ev is not None:
-            ev[2].record(stream)
-        for pt in parts_local:
-            if pt["reuse"]:
-                q, qb, kc, vc = pt["t"]
-                lib.reuse_sparse_attn(pt["p"], qb, kc, vc, pt["buf"].idx, pt["buf"].out_blk, stream)
-        if ev is not None:
-            ev[3].record(stream)
-
-    for _ in range(args.warmup):
-        flush.zero_()
-        step()
-    torch.cuda.synchronize(dev)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    clk = ClockSampler(local_rank)
-    with clk:
-        for i in range(args.steps):
-            flush.zero_()
-            step(evs[i])
-        torch.cuda.synchronize(dev)
-    clk.close()
-    if world > 1:
-        dist.barrier()
-    t_ref = [evs[i][0].elapsed_time(evs[i][1]) * 1e-3 for i in range(args.steps)]
-    t_sel = [evs[i][1].elapsed_time(evs[i][2]) * 1e-3 for i in range(args.steps)]
-    t_reu = [evs[i][2].elapsed_time(evs[i][3]) * 1e-3 for i in range(args.steps)]
-    t_step = [evs[i][0].elapsed_time(evs[i][3]) * 1e-3 for i in range(args.steps)]
+    # ---- eager per-kernel times, then the graph-replayed step (the `value`)
+    t_ref, t_sel, t_reu, t_step = time_eager(st, args.steps, args.warmup, flush)
     total_eager = sum(t_step)
-    total = total_eager
-    launch_mode = "eager"
-    if not args.no_graph:
-        # the step's launches captured once in a CUDA graph (requests/s
-        # without launch gaps); each replay is one full step on the same buffers
-        g = torch.cuda.CUDAGraph()
-        cs = torch.cuda.Stream(dev)
-        cs.wait_stream(torch.cuda.current_stream(dev))
-        with torch.cuda.stream(cs):
-            step()   # warm the capture stream
-        torch.cuda.current_stream(dev).wait_stream(cs)
-        torch.cuda.synchronize(dev)
-        with torch.cuda.graph(g, stream=cs):
-            step()
-        for _ in range(args.warmup):
-            flush.zero_()
-            g.replay()
-        torch.cuda.synchronize(dev)
-        gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-        clk = ClockSampler(local_rank)
-        with clk:
-            for i in range(args.steps):
-                flush.zero_()
-                gev[i][0].record(stream)
-                g.replay()
-                gev[i][1].record(stream)
-            torch.cuda.synchronize(dev)
-        clk.extend(g.replay, 0.25)
-        if world > 1:
-            dist.barrier()
-        total = sum(gev[i][0].elapsed_time(gev[i][1]) * 1e-3 for i in range(args.steps))
-        launch_mode = "cuda_graph"
-    tt = torch.tensor([total], dtype=torch.float64, device=dev)
+    g = capture_graph(st)
+    clk = ClockSampler(local_rank)
+    total = time_graph(st, g, args.steps, args.warmup, flush, clk, dist if world > 1 else None)
+    tt = torch.tensor([total], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     total_max = float(tt.item())
     reqs_per_step = glob.num_requests
     value = reqs_per_step * args.steps / total_max
+    rs = reuse_in_stream(st) if (rank == 0 and world == 1 and not st.mixed) else None
+    kern, flops, reuse_u = kernels_result(st, t_ref, t_sel, t_reu, tf_peak, hbm_peak, rs)
 
-    # ---- algorithmic work per launch
-    H, Hk, D = wl.num_heads, wl.num_kv_heads, wl.head_dim
-    g = H // Hk
-    flops_refresh = 0.0
-    reuse_bytes = reuse_logical = select_bytes = 0
-    total_idx_all = rows_all = 0
-    for pt in parts_local:
-        sub = pt["wl"]
-        kk, total_idx, rows, blk_rows = pt["p"].layout()
-        idx_host = pt["buf"].idx[:total_idx].cpu().numpy()
-        uniq_rows, off = 0, 0
-        for b in range(sub.num_requests):
-            rows_b = idx_host[off:off + H * kk[b]].reshape(H, kk[b])
-            off += H * kk[b]
-            for kv in range(Hk):
-                uniq_rows += len(np.unique(rows_b[kv * g:(kv + 1) * g])) + sub.blk[b]
-        if pt["reuse"]:
-            reuse_bytes += uniq_rows * 2 * D * 2 + 2 * blk_rows * H * D * 2 + 4 * total_idx
-            reuse_logical += sum(H * (sub.blk[b] + kk[b]) for b in range(sub.num_requests)) * 2 * D * 2 + \
-                2 * blk_rows * H * D * 2 + 4 * total_idx
-        if pt["refresh"]:
-            flops_refresh += sum(4.0 * H * L * L * D for L in sub.seq_len)
-            select_bytes += 4 * H * rows + 4 * total_idx
-        total_idx_all += total_idx
-        rows_all += rows
-    a_ref = flops_refresh / statistics.mean(t_ref) / 1e12 if flops_refresh else 0.0
-    a_reu = reuse_bytes / statistics.mean(t_reu) / 1e9 if reuse_bytes and not mixed else 0.0
-    a_sel = select_bytes / statistics.mean(t_sel) / 1e9 if select_bytes and not fused else 0.0
-    main_part = parts_local[0]
-    buf = main_part["buf"]
-    q, qb, kc, vc = main_part["t"]
-    p = main_part["p"]
-    k, total_idx, rows, blk_rows = p.layout()
-
-    # ---- all-gather of per-request outputs (NCCL), timed separately
-    allgather_ms = None
-    if world > 1 and len(parts_local) == 1:
-        counts_rows = [sum(glob.seq_len[i] for i in parts[r]) for r in range(world)]
-        counts_blk = [sum(glob.blk[i] for i in parts[r]) for r in range(world)]
-        for _ in range(2):
-            shard.allgather_outputs(buf.out, counts_rows)
-            shard.allgather_outputs(buf.out_blk, counts_blk)
-        torch.cuda.synchronize(dev)
-        dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        shard.allgather_outputs(buf.out, counts_rows)
-        shard.allgather_outputs(buf.out_blk, counts_blk)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        ag = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        dist.all_reduce(ag, op=dist.ReduceOp.MAX)
-        allgather_ms = float(ag.item())
+    # ---- multi-GPU: all-gather of the per-request outputs (serial and overlapped)
+    gather = None
+    if world > 1:
+        gather = gather_times(st, dist, shard, backend, g, flush, args)
 
     # ---- end to end through the public API with host buffers
-    pin = lambda t: t.pin_memory()  # noqa: E731
-    h_in, d_in, h_out, d_out = [], [], [], []
+    e2e = e2e_result(st, args, dist if world > 1 else None, backend)
+
+    # ---- CPU oracle baseline and the other configs (rank 0, N=1 only)
+    cpu = None
+    configs = None
+    if rank == 0 and world == 1:
+        if not args.no_cpu_baseline:
+            r, n, t, cores = cpu_oracle_rate(base, budget_s=12.0)
+            what = ("Refresh+importance+select+Reuse" if base.refresh_mask is None else
+                    "mixed: Refresh+importance+select for Refresh requests, Reuse for the rest, batch time "
+                    "extrapolated from per-kind means")
+            cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle",
+                   "sample": f"{n} request passes over the {base.num_requests} {base.name} requests ({what}, "
+                             f"all heads, fp64 numpy), {t:.1f} s"}
+        if not args.no_configs:
+            del g
+            configs = {}
+            for c in [x for x in ("C1", "C2", "C3", "C4") if x != args.config]:
+                try:
+                    configs[c] = config_result(c, dev, lib, synth, shard, tf_peak, hbm_peak, args.config_steps, 3,
+                                               flush)
+                except Exception as e:   # a sub-result must not lose the main line
+                    configs[c] = {"error": repr(e)}
+                torch.cuda.empty_cache()
+            try:
+                configs["N4_lm_head"] = lm_head_result(dev, lib, synth, tf_peak)
+            except Exception as e:
+                configs["N4_lm_head"] = {"error": repr(e)}
+
+    if rank == 0:
+        clocks = clk.summary()
+        if st.mixed:
+            km = kern["mixed"]
+            roof = {"bound": "tensor+hbm", "kernel": "dllm_mixed_attn (Refresh + Reuse, one launch)",
+                    "achieved": flops / (km["us"] * 1e-6) / 1e12, "peak": tf_peak,
+                    "unit": "TFLOP/s (Refresh FLOP / launch time)", "frac": km["frac"],
+                    "frac_definition": km["frac_definition"], "traffic": None,
+                    "peak_source": f"{peak_src} (MEASURED_PEAKS.json)"}
+        else:
+            kr = kern["refresh"]
+            roof = {"bound": "tensor", "kernel": "dllm_refresh_attn (tcgen05)", "achieved": kr["TFLOP/s"],
+                    "peak": tf_peak, "unit": "TFLOP/s", "frac": kr["frac"],
+                    "traffic": ncu_traffic("refresh", args.config),
+                    "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
+                    "frac_of_sustained": (kr["TFLOP/s"] / tf_sust) if tf_sust else None}
+        n_launch = 2 if st.mixed else sum(((2 if pc["refresh"] else 0) + (1 if pc["reuse"] else 0)) *
+                                          ((pc["wl"].num_requests + 255) // 256) for pc in st.pieces)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total_max / args.steps, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": workload_desc(base, world, args.scaling), "global_requests": reqs_per_step,
+                       "parallelism": f"request-sharded dp{world} (LPT), no data-path collective",
+                       "l2": "flushed before every step (512 MiB write, outside the step events)",
+                       "seed": synth.base_seed()},
+            "roofline": roof,
+            "kernels": kern,
+            "launch_mode": "cuda_graph",
+            "ms_per_step_eager": 1e3 * total_eager / args.steps,
+            "e2e": e2e,
+            "gpu_launches": n_launch * args.steps,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+            "allgather": gather,
+            "configs": configs,
+            "lib": lib.version(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _step_outputs(st, bufs=None):
+    """This rank's per-request outputs of one step, each the concatenation over its
+    requests (ascending): Refresh rows, new index lists (Refresh requests) and Reuse
+    rows; plus the per-global-request sizes of each (0 for requests without it)."""
+    n = st.glob.num_requests
+    sizes = {"out": [0] * n, "idx": [0] * n, "out_blk": [0] * n}
+    mine = st.parts[st.rank]
+    tensors = {"out": [], "idx": [], "out_blk": []}
+    bufs = bufs or [pc["buf"] for pc in st.pieces]
+    for pc, bf in zip(st.pieces, bufs):
+        sub = pc["wl"]
+        kk, total_idx, rows, blk_rows = pc["p"].layout()
+        H = sub.num_heads
+        gids = [mine[i] for i in range(len(mine)) if
+                (st.wl.refresh_mask is None or st.wl.refresh_mask[i] == pc["refresh"])]
+        if pc["refresh"]:
+            tensors["out"].append(bf.out[:rows])
+            tensors["idx"].append(bf.idx[:total_idx])
+            for j, gi in enumerate(gids):
+                sizes["out"][gi] = sub.seq_len[j]
+                sizes["idx"][gi] = H * kk[j]
+        if pc["reuse"]:
+            tensors["out_blk"].append(bf.out_blk[:blk_rows])
+            for j, gi in enumerate(gids):
+                sizes["out_blk"][gi] = sub.blk[j]
+    # every rank computes every rank's sizes (shapes are known from the workload)
+    for name in sizes:
+        for r, part in enumerate(st.parts):
+            if r == st.rank:
+                continue
+            sub_r = st.synth.subset(st.glob, part)
+            for j, gi in enumerate(part):
+                m = None if st.glob.refresh_mask is None else st.glob.refresh_mask[gi]
+                blk = sub_r.blk[j]
+                L = sub_r.seq_len[j]
+                k = st.lib.keep_count(st.glob.keep_ratio, L - blk)
+                if name == "out" and m is not False:
+                    sizes[name][gi] = L
+                elif name == "idx" and m is not False:
+                    sizes[name][gi] = st.glob.num_heads * k
+                elif name == "out_blk" and m is not True:
+                    sizes[name][gi] = blk
+    torch = st.torch
+    cat = {k: (torch.cat(v) if v else None) for k, v in tensors.items()}
+    return cat, sizes
+
+
+def gather_times(st, dist, shard, backend, g, flush, args):
+    """NCCL all-gather of one step's per-request outputs to every rank: serial time
+    (gather alone) and the per-step time when step i's gather overlaps step i+1's
+    compute on a side stream (max over ranks)."""
+    torch = st.torch
+    dev = st.dev
+    outs, sizes = _step_outputs(st)
+    counts = {k: [sum(sizes[k][i] for i in p) for p in st.parts] for k in sizes}
+
+    def gather_all():
+        res = {}
+        for k, t in outs.items():
+            if sum(counts[k]) == 0:
+                continue
+            loc = t if t is not None else torch.zeros((0,), device=dev)
+            if backend != "nccl":
+                loc = loc.cpu()
+            if loc.dim() > 1:
+                loc = loc.reshape(loc.shape[0], -1)
+            res[k] = shard.allgather_outputs(loc, counts[k])
+        return res
+
+    for _ in range(2):
+        gather_all()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    gathered = gather_all()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    serial_ms = e0.elapsed_time(e1)
+    # overlapped: the gather of step i (side stream) beside the compute of step i+1
+    side = torch.cuda.Stream(dev)
+    steps = max(3, min(args.steps, 10))
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0.record()
+    for _ in range(steps):
+        done = torch.cuda.Event()
+        g.replay()
+        done.record()
+        side.wait_event(done)
+        with torch.cuda.stream(side):
+            gather_all()
+    torch.cuda.current_stream(dev).wait_stream(side)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ovl_ms = e0.elapsed_time(e1) / steps
+    t = torch.tensor([serial_ms, ovl_ms], dtype=torch.float64)
+    if backend == "nccl":
+        t = t.to(dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    # reassembly check: every rank holds the global outputs in request order
+    n_ok = 0
+    for k, gt in gathered.items():
+        per_req = shard.reassemble(gt, st.parts, sizes[k])
+        n_ok += sum(1 for x in per_req if x is not None)
+    nbytes = {k: sum(counts[k]) * (outs[k][0].numel() * outs[k].element_size() if outs[k] is not None and
+                                   outs[k].shape[0] else 0) for k in counts}
+    return {"serial_ms": float(t[0]), "overlapped_ms_per_step": float(t[1]),
+            "gathered": sorted(gathered), "bytes_gathered_per_rank": int(sum(nbytes.values())),
+            "backend": backend, "requests_reassembled": n_ok,
+            "note": "serial: all outputs of one step gathered alone; overlapped: per-step time with step i's "
+                    "gather on a side stream beside step i+1's graph replay"}
+
+
+def e2e_result(st, args, dist, backend):
+    """The metric through the public API from pinned HOST buffers: each step copies
+    its inputs to the device and its outputs back, pipelined the way a serving loop
+    runs them (step i's read-back on a second stream beside step i+1's input copy)."""
+    torch = st.torch
+    dev = st.dev
+    stream = torch.cuda.current_stream(dev)
+    h_in, d_in, d_out = [], [], []
     seen = set()
 
     def add_in(host, dev_t):
         if id(dev_t) not in seen:    # a mixed batch's phases share one cache: copied once
             seen.add(id(dev_t))
-            h_in.append(pin(host))
+            h_in.append(host.pin_memory())
             d_in.append(dev_t)
 
-    for pt in parts_local:
-        ht, tb, (_, tidx, _, _) = pt["host"], pt["buf"], pt["p"].layout()
-        add_in(ht["k_cache"], pt["t"][2])
-        add_in(ht["v_cache"], pt["t"][3])
-        if pt["reuse"]:
-            add_in(ht["q_blk"], pt["t"][1])
+    for pc in st.pieces:
+        ht, tb, (_, tidx, _, _) = pc["host"], pc["buf"], pc["p"].layout()
+        add_in(ht["k_cache"], pc["t"][2])
+        add_in(ht["v_cache"], pc["t"][3])
+        if pc["reuse"]:
+            add_in(ht["q_blk"], pc["t"][1])
             d_out.append(tb.out_blk)
-        if pt["refresh"]:
-            add_in(ht["q"], pt["t"][0])
+        if pc["refresh"]:
+            add_in(ht["q"], pc["t"][0])
             d_out += [tb.out, tb.idx[:max(tidx, 1)]]
         else:
-            # reuse-only requests bring the index lists of their earlier selection
             h_in.append(tb.idx[:max(tidx, 1)].cpu().pin_memory())
             d_in.append(tb.idx[:max(tidx, 1)])
     h_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in d_out]
     h2d = sum(t.numel() * t.element_size() for t in h_in)
     d2h = sum(t.numel() * t.element_size() for t in h_out)
-
-    # Steps are pipelined the way a serving loop runs them: step i's results go back
-    # to the host on a second stream (the D2H copy engine) while step i+1's inputs
-    # come in on the compute stream (the H2D engine); step i+1's kernels wait for
-    # both (its inputs, and the read-out of the output buffers they overwrite).
     d2h_stream = torch.cuda.Stream(dev)
     d2h_done = [None]
 
@@ -552,7 +853,7 @@ def main():
             d.copy_(h, non_blocking=True)
         if d2h_done[0] is not None:
             stream.wait_event(d2h_done[0])
-        step()
+        st.step()
         computed = torch.cuda.Event()
         computed.record(stream)
         d2h_stream.wait_event(computed)
@@ -564,7 +865,7 @@ def main():
 
     e2e_step()
     torch.cuda.synchronize(dev)
-    if world > 1:
+    if dist is not None:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -573,84 +874,14 @@ def main():
     stream.wait_event(d2h_done[0])      # the last step's results are on the host
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    te = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device=dev)
-    if world > 1:
+    te = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64)
+    if dist is not None:
+        if backend == "nccl":
+            te = te.to(dev)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = reqs_per_step * args.e2e_steps / float(te.item())
-
-    # ---- CPU oracle baseline (rank 0, N=1 only)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r, n, t, cores = cpu_oracle_rate(base, budget_s=12.0)
-        what = ("Refresh+importance+select+Reuse" if base.refresh_mask is None else
-                "mixed: Refresh+importance+select for Refresh requests, Reuse for the rest, batch time "
-                "extrapolated from per-kind means")
-        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{n} request passes over the {base.num_requests} {base.name} requests ({what}, "
-                         f"all heads, fp64 numpy), {t:.1f} s"}
-
-    if rank == 0:
-        clocks = clk.summary()
-        traffic = ncu_traffic("refresh", args.config)
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * total_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": workload_desc(base, world), "global_requests": reqs_per_step,
-                       "parallelism": f"request-sharded dp{world} (LPT), no data-path collective",
-                       "l2": "flushed before every step (512 MiB write, outside the step events)",
-                       "seed": synth.base_seed()},
-            "roofline": ({"bound": "tensor", "kernel": ("dllm_refresh_select_attn (tcgen05 Refresh + select in one "
-                                                        "call: FLOP of Refresh only / time of both)") if fused else
-                          "dllm_refresh_attn (tcgen05)", "achieved": a_ref,
-                          "peak": tf_peak, "unit": "TFLOP/s", "frac": a_ref / tf_peak, "traffic": traffic,
-                          "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
-                          "frac_of_sustained": (a_ref / tf_sust) if tf_sust else None} if not mixed else
-                         {"bound": "tensor+hbm", "kernel": "dllm_mixed_attn (Refresh + Reuse, one launch)",
-                          "achieved": a_ref, "peak": tf_peak, "unit": "TFLOP/s (Refresh FLOP / launch time)",
-                          "frac": (flops_refresh / (tf_peak * 1e12) + reuse_bytes / (hbm_peak * 1e9))
-                          / statistics.mean(t_ref),
-                          "frac_definition": "additive roofline time (Refresh FLOP / bf16 peak + Reuse unique "
-                                             "bytes / HBM peak) / measured launch time", "traffic": None,
-                          "peak_source": f"{peak_src} (MEASURED_PEAKS.json)"}),
-            "kernels": ({
-                "mixed": {"us": 1e6 * statistics.mean(t_ref), "refresh_flop": flops_refresh,
-                          "reuse_bytes_unique": reuse_bytes, "reuse_bytes_logical": reuse_logical,
-                          "roofline_us": 1e6 * (flops_refresh / (tf_peak * 1e12) + reuse_bytes / (hbm_peak * 1e9))},
-                "select": ({"in_one_call_with": "Refresh (timed with it)", "fused_in_kernel": fused_in_kernel,
-                            "bytes_per_launch": select_bytes}
-                           if fused else {"us": 1e6 * statistics.mean(t_sel), "GB/s": a_sel, "frac": a_sel / hbm_peak,
-                                          "bytes_per_launch": select_bytes})} if mixed else {
-                "refresh": {"us": 1e6 * statistics.mean(t_ref), "TFLOP/s": a_ref, "frac": a_ref / tf_peak,
-                            "flop_per_launch": flops_refresh},
-                "select": ({"in_one_call_with": "Refresh (timed with it)", "fused_in_kernel": fused_in_kernel,
-                            "bytes_per_launch": select_bytes}
-                           if fused else {"us": 1e6 * statistics.mean(t_sel), "GB/s": a_sel, "frac": a_sel / hbm_peak,
-                                          "bytes_per_launch": select_bytes}),
-                "reuse": {"us": 1e6 * statistics.mean(t_reu), "GB/s": a_reu, "frac": a_reu / hbm_peak,
-                          "bytes_per_launch_unique": reuse_bytes, "bytes_per_launch_logical": reuse_logical,
-                          "GB/s_logical": reuse_logical / statistics.mean(t_reu) / 1e9, "bound": "hbm",
-                          "peak": hbm_peak},
-                "block_cycle_us": (1e6 * (statistics.mean(t_ref) + statistics.mean(t_sel) + 31 * statistics.mean(t_reu))
-                                   if len(parts_local) == 1 and parts_local[0]["refresh"] else None),
-            }),
-            "launch_mode": launch_mode,
-            "ms_per_step_eager": 1e3 * total_eager / args.steps,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "steps": args.e2e_steps, "pipelining": "D2H of step i on a second stream beside the H2D of step i+1"},
-            "select_fused": fused_in_kernel,
-            "gpu_launches": ((1 if fused_in_kernel else 2) if mixed else
-                             sum(((1 if fused_in_kernel else 2) * pt["refresh"] + pt["reuse"]) * ((pt["wl"].num_requests + 255) // 256)
-                                                 for pt in parts_local)) * args.steps,
-            "clocks": clocks,
-            "cpu_baseline": cpu,
-            "allgather_ms": allgather_ms,
-            "lib": lib.version(),
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    return {"value": st.glob.num_requests * args.e2e_steps / float(te.item()), "unit": UNIT,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+            "pipelining": "D2H of step i on a second stream beside the H2D of step i+1"}
 
 
 if __name__ == "__main__":

@@ -17,14 +17,27 @@ from typing import List, Sequence
 import torch
 
 
-def request_cost(L: int, blk: int, H: int, H_kv: int, D: int, k: int, refresh: bool = True,
+def request_cost(L: int, blk: int, H: int, H_kv: int, D: int, k: int, refresh: bool = True, reuse: bool = True,
                  tflops: float = 1642.7, gbs: float = 6468.9) -> float:
-    """Estimated seconds of one request on one GPU (roofline estimate)."""
+    """Estimated seconds of one request on one GPU (roofline estimate): Refresh
+    FLOPs at the tensor peak and/or Reuse bytes at HBM bandwidth."""
     t = 0.0
     if refresh:
         t += 4.0 * H * L * L * D / (tflops * 1e12)
-    t += (H * (blk + k) * 2 * D * 2 + 2 * H * blk * D * 2) / (gbs * 1e9)
+    if reuse:
+        t += (H * (blk + k) * 2 * D * 2 + 2 * H * blk * D * 2) / (gbs * 1e9)
     return t
+
+
+def workload_costs(wl, k_per_request: Sequence[int]) -> List[float]:
+    """Per-request cost estimates of one step of ``wl``: without a refresh_mask every
+    request runs Refresh + select + Reuse; with one (a mixed burst batch, DESIGN.md
+    R20) a Refresh request runs Refresh + select and a Reuse request Reuse only."""
+    mask = wl.refresh_mask
+    return [request_cost(L, e - s, wl.num_heads, wl.num_kv_heads, wl.head_dim, k,
+                         refresh=True if mask is None else bool(mask[i]),
+                         reuse=True if mask is None else not mask[i])
+            for i, (L, s, e, k) in enumerate(zip(wl.seq_len, wl.blk_start, wl.blk_end, k_per_request))]
 
 
 def lpt_partition(costs: Sequence[float], n: int) -> List[List[int]]:
@@ -65,3 +78,19 @@ def efficiency(costs: Sequence[float], n: int) -> float:
     parts = lpt_partition(costs, n)
     ms = makespan(costs, parts)
     return (sum(costs) / n) / ms if ms > 0 else 1.0
+
+
+def reassemble(gathered: torch.Tensor, parts: List[List[int]], sizes: Sequence[int]) -> List[torch.Tensor]:
+    """Per-request outputs in GLOBAL request order from an all-gathered tensor.
+
+    Rank r contributed its requests ``parts[r]`` (ascending) back to back along dim
+    0, request i taking ``sizes[i]`` rows (0 for requests without this output);
+    ``gathered`` is the rank-order concatenation (``allgather_outputs``)."""
+    out: List[torch.Tensor] = [None] * len(sizes)   # type: ignore[list-item]
+    off = 0
+    for p in parts:
+        for i in p:
+            out[i] = gathered[off:off + sizes[i]]
+            off += sizes[i]
+    assert off == gathered.shape[0], (off, gathered.shape)
+    return out
