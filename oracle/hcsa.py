@@ -42,11 +42,14 @@ __all__ = [
     "select_heads",
     "score_global",
     "select_global",
+    "score_groups",
+    "select_groups",
     "attention_with_cache",
     "attention_masked_dense",
     "refresh_batch",
     "select_batch",
     "select_global_batch",
+    "select_groups_batch",
     "reuse_batch",
 ]
 
@@ -274,6 +277,35 @@ def select_global(Q_blk, K, seq_len: int, blk_start: int, blk_end: int,
     return C[select_topk(score_global(Q_blk, _f64(K)[C], window), k)]
 
 
+def score_groups(Q_blk, K, window: int, num_kv_heads: int) -> np.ndarray:
+    """Per-KV-group scores S_g[j] = sum_{h in g} max_{m in win(j)} Q_{b,h} . K_{m,kv(h)}.
+
+    Eq. 5 (§2.4) restricted to the query heads that share one
+    KV head (GQA, R10, R21): the per-head pooled importance of Eq. 6
+     summed over the group g = {h : kv(h) = g}.  Returns
+    [H_kv, n] for the candidate rows K.  With H_kv = H it is the per-head Eq. 6
+    score; with H_kv = 1 it is Eq. 5.
+    """
+    pooled = pool_scores(raw_scores(Q_blk, K), window)
+    H = pooled.shape[0]
+    return np.stack([pooled[[h for h in range(H) if kv_head(h, H, num_kv_heads) == g]].sum(axis=0)
+                     for g in range(num_kv_heads)])
+
+
+def select_groups(Q_blk, K, seq_len: int, blk_start: int, blk_end: int,
+                  keep_ratio: float, window: int, num_kv_heads: int) -> np.ndarray:
+    """One index set per KV group (next row N2): I_g = TopK(S_g, k) with the
+    per-head rules (k = keep_count, R5; ties to the lower index, R6; ascending,
+    R7), every head of group g reading I_g (§4.5: rL positions
+    per head; here shared by the heads that share the KV rows).  [H_kv, k]."""
+    C = candidates(seq_len, blk_start, blk_end)
+    k = keep_count(keep_ratio, len(C))
+    if k == 0:
+        return np.zeros((num_kv_heads, 0), dtype=np.int64)
+    S = score_groups(Q_blk, _f64(K)[C], window, num_kv_heads)
+    return C[select_topk(S, k)]
+
+
 # ----------------------------------------------------------------------------
 # Eq. 4 — Reuse sparse attention
 # ----------------------------------------------------------------------------
@@ -390,6 +422,26 @@ def select_global_batch(scores, seq_len, blk_start, blk_end, keep_ratio: float, 
             out.append(np.zeros((0,), np.int64))
             continue
         S = pool_scores(_f64(sc)[:, C], window).sum(axis=0)
+        out.append(C[select_topk(S, k)])
+    return out
+
+
+def select_groups_batch(scores, seq_len, blk_start, blk_end, keep_ratio: float, window: int,
+                        num_kv_heads: int):
+    """Per-KV-group selection from precomputed raw scores [H, L_b] (score_groups
+    on the candidate axis, one top-k per group).  Returns a list of [H_kv, k_b]
+    int64 position arrays."""
+    out = []
+    for b, sc in enumerate(scores):
+        C = candidates(seq_len[b], blk_start[b], blk_end[b])
+        k = keep_count(keep_ratio, len(C))
+        if k == 0:
+            out.append(np.zeros((num_kv_heads, 0), np.int64))
+            continue
+        pooled = pool_scores(_f64(sc)[:, C], window)
+        H = pooled.shape[0]
+        S = np.stack([pooled[[h for h in range(H) if kv_head(h, H, num_kv_heads) == g]].sum(axis=0)
+                      for g in range(num_kv_heads)])
         out.append(C[select_topk(S, k)])
     return out
 

@@ -281,3 +281,50 @@ def test_select_global_batch_pins():
     g1 = O.select_global_batch(sc, [50], [10], [20], 0.4, 3)[0]
     g2 = O.select_global_batch([sc[0][::-1]], [50], [10], [20], 0.4, 3)[0]
     assert np.array_equal(g1, g2)
+
+
+# ---------------------------------------------------------------- N2: per-KV-group selection
+def test_select_groups_reduces_to_per_head_and_uniform():
+    """score_groups sums Eq. 6's pooled scores over the heads sharing a KV head:
+    with H_kv = H each group is one head (per-head Eq. 6 selection),
+    with H_kv = 1 the group is every head (Eq. 5)."""
+    rng = np.random.default_rng(7)
+    L, bs, be, D = 37, 20, 25, 8
+    Qb = rng.integers(-3, 4, size=(be - bs, 4, D)).astype(np.float64)
+    K4 = rng.integers(-3, 4, size=(L, 4, D)).astype(np.float64)
+    per_head = O.select_heads(Qb, K4, L, bs, be, 0.3, 3)
+    assert np.array_equal(O.select_groups(Qb, K4, L, bs, be, 0.3, 3, 4), per_head)
+    K1 = K4[:, :1]
+    assert np.array_equal(O.select_groups(Qb, K1, L, bs, be, 0.3, 3, 1)[0],
+                          O.select_global(Qb, K1, L, bs, be, 0.3, 3))
+
+
+def test_select_groups_hand_worked():
+    """H = 4 query heads over H_kv = 2 KV heads, w = 1, r = 0.5 on 4 candidates
+    (k = 2), raw scores given: group 0 = heads {0, 1}: S = [4,0,0,1] + [0,3,2,1]
+    = [4,3,2,2] -> {0, 1}; group 1 = heads {2, 3}: S = [0,0,5,0] + [1,1,0,4] =
+    [1,1,5,4] -> {2, 3}.  (Per head the sets would be {0,3}, {1,2}, {0,2}, {0,3}.)"""
+    raw = np.array([[4, 0, 0, 1, 9], [0, 3, 2, 1, 9], [0, 0, 5, 0, 9], [1, 1, 0, 4, 9]], dtype=np.float64)
+    got = O.select_groups_batch([raw], [5], [4], [5], 0.5, 1, 2)[0]
+    assert got.tolist() == [[0, 1], [2, 3]]
+    per_head = O.select_batch([raw], [5], [4], [5], 0.5, 1)[0]
+    assert per_head.tolist() == [[0, 3], [1, 2], [0, 2], [0, 3]]
+
+
+def test_select_groups_batch_brute_force():
+    """Against brute force over all k-subsets of each group's summed pooled scores
+    (largest sum, ties to the lexicographically smallest subset)."""
+    from itertools import combinations
+    rng = np.random.default_rng(11)
+    H, Hk, L, bs, be = 6, 2, 12, 3, 5
+    raw = rng.integers(-2, 3, size=(H, L)).astype(np.float64)
+    got = O.select_groups_batch([raw], [L], [bs], [be], 0.4, 3, Hk)[0]
+    C = np.r_[0:bs, be:L]
+    k = O.keep_count(0.4, len(C))
+    for g in range(Hk):
+        S = np.zeros(len(C))
+        for h in range(g * H // Hk, (g + 1) * H // Hk):
+            r = raw[h, C]
+            S += [max(r[max(0, j - 1):j + 2]) for j in range(len(C))]
+        best = min(combinations(range(len(C)), k), key=lambda s: (-sum(S[list(s)]), s))
+        assert got[g].tolist() == C[list(best)].tolist()
