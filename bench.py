@@ -255,8 +255,9 @@ class Step:
     """The batch of this rank (an LPT shard of `glob`), its problems / buffers and
     the step closure."""
 
-    def __init__(self, glob, parts, rank, dev, lib, synth):
+    def __init__(self, glob, parts, rank, dev, lib, synth, select="heads"):
         import torch
+        self.select = select   # "heads" (Eq. 6 per query head) or "groups" (N2: one set per KV group)
         self.torch, self.lib, self.synth, self.dev = torch, lib, synth, dev
         self.glob, self.parts, self.rank = glob, parts, rank
         wl = synth.subset(glob, parts[rank])
@@ -338,7 +339,8 @@ class Step:
         rec(1)
         for pc, bf in zip(self.pieces, bufs):
             if pc["refresh"]:
-                lib.select_heads(pc["p"], bf.scores, bf.idx, stream)
+                (lib.select_groups if self.select == "groups" else lib.select_heads)(pc["p"], bf.scores, bf.idx,
+                                                                                    stream)
         rec(2)
         for pc, bf in zip(self.pieces, bufs):
             if pc["reuse"]:
@@ -547,17 +549,19 @@ def kernels_result(st, t_ref, t_sel, t_reu, tf_peak, hbm_peak, reuse_stream_s=No
     return out, flops, reuse_u
 
 
-def config_result(cfg_name, dev, lib, synth, shard, tf_peak, hbm_peak, steps, warmup, flush):
+def config_result(cfg_name, dev, lib, synth, shard, tf_peak, hbm_peak, steps, warmup, flush, select="heads"):
     """A sub-result for `configs`: one GPU, the whole config batch."""
     wl = synth.config(cfg_name)
-    st = Step(wl, [list(range(wl.num_requests))], 0, dev, lib, synth)
+    st = Step(wl, [list(range(wl.num_requests))], 0, dev, lib, synth, select)
     t_ref, t_sel, t_reu, t_step = time_eager(st, steps, warmup, flush)
     g = capture_graph(st)
     total = time_graph(st, g, steps, warmup, flush)
     rs = None if st.mixed else reuse_in_stream(st)
     kern, flops, reuse_u = kernels_result(st, t_ref, t_sel, t_reu, tf_peak, hbm_peak, rs)
     del g
-    return {"workload": workload_desc(wl, 1, "weak"), "requests_per_s": wl.num_requests * steps / total,
+    return {"workload": workload_desc(wl, 1, "weak") + ("" if select == "heads" else
+                                                       ", selection: one set per KV group (dllm_select_groups)"),
+            "requests_per_s": wl.num_requests * steps / total,
             "ms_per_step": 1e3 * total / steps, "launch_mode": "cuda_graph", "kernels": kern}
 
 
@@ -650,6 +654,12 @@ def main():
                 except Exception as e:   # a sub-result must not lose the main line
                     configs[c] = {"error": repr(e)}
                 torch.cuda.empty_cache()
+            try:   # next row N2: the Dream GQA shape with one index set per KV group
+                configs["C2_groups"] = config_result("C2", dev, lib, synth, shard, tf_peak, hbm_peak,
+                                                     args.config_steps, 3, flush, select="groups")
+            except Exception as e:
+                configs["C2_groups"] = {"error": repr(e)}
+            torch.cuda.empty_cache()
             try:
                 configs["N4_lm_head"] = lm_head_result(dev, lib, synth, tf_peak)
             except Exception as e:

@@ -158,6 +158,18 @@ DLLM_API int dllm_refresh_select_attn(const dllm_problem *p, const void *q, cons
  * the head sums are exact in fp32.  scores, idx: DEVICE. */
 DLLM_API int dllm_select_global(const dllm_problem *p, const float *scores, int32_t *idx, void *stream);
 
+/* Per-KV-group selection (next row N2, GQA): for every request and KV head g,
+ * S_g[c] = sum over the query heads h with kv(h) = g (ascending h, fp32) of the
+ * per-head pooled score (Eq. 6's pooling), i.e. Eq. 5
+ * restricted to the heads sharing one KV head (DESIGN.md
+ * R21); ONE top-k set per (request, KV head) with the per-head rules (k_b, ties
+ * to the lower candidate, ascending positions), written to the idx slot of every
+ * head of the group, so dllm_reuse_sparse_attn reads each group's K/V rows once
+ * per head from the same positions.  H_kv = H gives dllm_select_heads, H_kv = 1
+ * dllm_select_global.  Bit-exact when the head sums are exact in fp32.  scores,
+ * idx: DEVICE. */
+DLLM_API int dllm_select_groups(const dllm_problem *p, const float *scores, int32_t *idx, void *stream);
+
 /* Reuse (Eq. 4): out_blk[q, h] = softmax_j(tau * Qb[q,h].K[j,kv(h)]) . V[j,kv(h)]
  * over J^h = [bs, be) ++ idx(b, h), K/V read in place through the block table
  * (no pack, no copy).  The caller has written the active block's K/V rows

@@ -24,7 +24,7 @@
 namespace dllm {
 cudaError_t launch_select(const Plan &, const float *, int32_t *, cudaStream_t);
 cudaError_t launch_check_indices(const Plan &, const int32_t *, int32_t *, cudaStream_t);
-cudaError_t launch_select_global(const Plan &, const float *, int32_t *, cudaStream_t);
+cudaError_t launch_select_global(const Plan &, const float *, int32_t *, int, cudaStream_t);
 cudaError_t launch_reuse_packed(const Plan &, const void *, const void *, const void *, const void *, const void *,
                                 void *, cudaStream_t);
 cudaError_t launch_pack_kv(const Plan &, const void *, const void *, const int32_t *, void *, void *, cudaStream_t);
@@ -348,25 +348,40 @@ int dllm_select_heads(const dllm_problem *p, const float *scores, int32_t *idx, 
   return ok();
 }
 
-int dllm_select_global(const dllm_problem *p, const float *scores, int32_t *idx, void *stream) {
+}  // extern "C"
+
+namespace {
+int select_sets(const dllm_problem *p, const float *scores, int32_t *idx, void *stream, int heads_per_set,
+                const char *who) {
   Layout lay;
   int st = make_layout(p, lay);
   if (st) return st;
   const int B = p->num_requests;
   if (B == 0) return ok();
-  if (!scores || !idx) return fail(DLLM_ERR_INVALID_ARG, "select_global: NULL pointer");
+  if (!scores || !idx) return fail(DLLM_ERR_INVALID_ARG, "%s: NULL pointer", who);
   for (int b = 0; b < B; ++b)
     if (p->seq_len[b] > DLLM_MAX_SELECT_LEN)
-      return fail(DLLM_ERR_UNSUPPORTED, "select_global: request %d seq_len=%d > %d", b, p->seq_len[b],
-                  DLLM_MAX_SELECT_LEN);
+      return fail(DLLM_ERR_UNSUPPORTED, "%s: request %d seq_len=%d > %d", who, b, p->seq_len[b], DLLM_MAX_SELECT_LEN);
   static thread_local Plan pl;
   for (int b0 = 0; b0 < B; b0 += kMaxReqPerLaunch) {
     const int b1 = b0 + kMaxReqPerLaunch < B ? b0 + kMaxReqPerLaunch : B;
     fill_plan(pl, p, lay.k, b0, b1, lay.cu_L, lay.cu_blk, lay.cu_k, [&](int) { return 1; });
-    cudaError_t e = launch_select_global(pl, scores, idx, (cudaStream_t)stream);
+    cudaError_t e = launch_select_global(pl, scores, idx, heads_per_set, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "select_global launch");
   }
   return ok();
+}
+}  // namespace
+
+extern "C" {
+
+int dllm_select_global(const dllm_problem *p, const float *scores, int32_t *idx, void *stream) {
+  return select_sets(p, scores, idx, stream, p ? p->num_heads : 1, "select_global");
+}
+
+int dllm_select_groups(const dllm_problem *p, const float *scores, int32_t *idx, void *stream) {
+  return select_sets(p, scores, idx, stream, p && p->num_kv_heads > 0 ? p->num_heads / p->num_kv_heads : 1,
+                     "select_groups");
 }
 
 int dllm_reuse_sparse_attn(const dllm_problem *p, const void *q_blk, const void *k_cache, const void *v_cache,

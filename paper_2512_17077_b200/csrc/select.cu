@@ -214,31 +214,37 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
   SEL_TR(9);
 }
 
-// Uniform (global) selection, the Sparse-dLLM baseline of PAPER.md:136-145
-// (§2.4, Eq. 5): S[c] = sum over heads (ascending h, fp32) of the per-head pooled
-// score, one top-k per request with the same radix select / tie rule, and the
-// shared index set is written to EVERY head's slot of the idx layout so that
-// dllm_reuse_sparse_attn consumes it unchanged.  One CTA per request.
+// Set selection over a group of heads (next row N2):
+//  * uniform, the Sparse-dLLM baseline of PAPER.md:136-145 (§2.4, Eq. 5): the set
+//    is every head of the request;
+//  * per KV group (GQA): the set is the H / H_kv query heads sharing one KV head
+//    (Eq. 5 restricted to the group, R21).
+// S[c] = sum over the set's heads (ascending h, fp32) of the per-head pooled score,
+// one top-k per (request, set) with the same radix select / tie rule, and the
+// shared index set is written to every head's slot of the idx layout so that
+// dllm_reuse_sparse_attn consumes it unchanged.  One CTA per (request, set).
 __global__ void __launch_bounds__(kSelThreads)
 select_global_kernel(const __grid_constant__ Plan plan, const float *__restrict__ scores,
-                     int32_t *__restrict__ idx) {
+                     int32_t *__restrict__ idx, const int heads_per_set) {
   extern __shared__ uint32_t keys[];                  // [n_ctx]
   __shared__ int hist[256];
   __shared__ int warp_buf[32];
   __shared__ uint32_t s_prefix;
   __shared__ int s_krem;
-  const ReqInfo &R = plan.r[blockIdx.x];
+  // CTA = (request, head set): the set's heads are [h0, h0 + heads_per_set)
+  const int sets = plan.H / heads_per_set;
+  const ReqInfo &R = plan.r[blockIdx.x / sets];
+  const int h0 = (blockIdx.x % sets) * heads_per_set;
   const int L = R.L, bs = R.bs, blk = R.be - R.bs;
   const int n = L - blk;
   const int k = R.k;
   if (k <= 0) return;
-  const int H = plan.H;
   const float *raw0 = scores + R.score_off;
   const int half = plan.window >> 1;
   for (int c = threadIdx.x; c < n; c += kSelThreads) {
     const int lo = max(0, c - half), hi = min(n - 1, c + half);
     float acc = 0.f;
-    for (int h = 0; h < H; ++h) {
+    for (int h = h0; h < h0 + heads_per_set; ++h) {
       const float *raw = raw0 + (int64_t)h * L;
       float m = -INFINITY;
       for (int j = lo; j <= hi; ++j) m = fmaxf(m, __ldg(raw + (j < bs ? j : j + blk)));
@@ -310,7 +316,7 @@ select_global_kernel(const __grid_constant__ Plan plan, const float *__restrict_
     if (gt || (eq && eq_pre < krem)) {
       const int pos = c < bs ? c : c + blk;
       const int pos_out = gt_pre + min(eq_pre, krem);
-      for (int h = 0; h < H; ++h) out0[(int64_t)h * k + pos_out] = pos;
+      for (int h = h0; h < h0 + heads_per_set; ++h) out0[(int64_t)h * k + pos_out] = pos;
     }
     gt_base += tot & 0xffff;
     eq_base += tot >> 16;
@@ -354,7 +360,8 @@ cudaError_t launch_select(const Plan &plan, const float *scores, int32_t *idx, c
                     stage);
 }
 
-cudaError_t launch_select_global(const Plan &plan, const float *scores, int32_t *idx, cudaStream_t st) {
+cudaError_t launch_select_global(const Plan &plan, const float *scores, int32_t *idx, int heads_per_set,
+                                 cudaStream_t st) {
   int max_n = 0;
   for (int b = 0; b < plan.nreq; ++b) max_n = max(max_n, plan.r[b].L - (plan.r[b].be - plan.r[b].bs));
   const size_t smem = (size_t)max(max_n, 1) * sizeof(uint32_t);
@@ -366,7 +373,8 @@ cudaError_t launch_select_global(const Plan &plan, const float *scores, int32_t 
   });
   if (attr != cudaSuccess) return attr;
   if (smem > (size_t)kSelSmemMaxWords * sizeof(uint32_t)) return cudaErrorInvalidValue;
-  select_global_kernel<<<plan.nreq, kSelThreads, smem, st>>>(plan, scores, idx);
+  select_global_kernel<<<plan.nreq * (plan.H / heads_per_set), kSelThreads, smem, st>>>(plan, scores, idx,
+                                                                                        heads_per_set);
   return cudaGetLastError();
 }
 

@@ -26,7 +26,8 @@ DLLM_ERR_SHAPE = -3
 DLLM_ERR_K_RANGE = -4
 DLLM_ERR_CUDA = -5
 
-EXPORTED = ("dllm_workspace_bytes", "dllm_keep_count", "dllm_index_layout", "dllm_refresh_attn", "dllm_select_heads", "dllm_select_global",
+EXPORTED = ("dllm_workspace_bytes", "dllm_keep_count", "dllm_index_layout", "dllm_refresh_attn", "dllm_select_heads",
+            "dllm_select_global", "dllm_select_groups",
             "dllm_refresh_select_attn", "dllm_mixed_select_attn",
             "dllm_reuse_sparse_attn", "dllm_pack_kv", "dllm_reuse_packed", "dllm_mixed_attn", "dllm_logit_chunks",
             "dllm_lm_head_workspace_bytes", "dllm_lm_head_argmax", "dllm_check_indices", "dllm_status_string",
@@ -80,6 +81,9 @@ def _load() -> ctypes.CDLL:
     lib.dllm_select_heads.restype = ctypes.c_int
     lib.dllm_select_global.argtypes = [P, vp, vp, vp]
     lib.dllm_select_global.restype = ctypes.c_int
+    if hasattr(lib, "dllm_select_groups"):
+        lib.dllm_select_groups.argtypes = [P, vp, vp, vp]
+        lib.dllm_select_groups.restype = ctypes.c_int
     lib.dllm_reuse_sparse_attn.argtypes = [P, vp, vp, vp, vp, vp, vp]
     lib.dllm_reuse_sparse_attn.restype = ctypes.c_int
     lib.dllm_pack_kv.argtypes = [P, vp, vp, vp, vp, vp, vp]
@@ -289,6 +293,13 @@ def select_global(p: Problem, scores, idx, stream=None) -> None:
     _, ns, ni, _ = _sizes(p)
     _check(_lib.dllm_select_global(p.ref, _dev(scores, "scores", torch.float32, ns),
                                    _dev(idx, "idx", torch.int32, ni), _stream(stream)), "dllm_select_global")
+
+
+def select_groups(p: Problem, scores, idx, stream=None) -> None:
+    """dllm_select_groups (N2, GQA: one shared set per KV group)."""
+    _, ns, ni, _ = _sizes(p)
+    _check(_lib.dllm_select_groups(p.ref, _dev(scores, "scores", torch.float32, ns),
+                                   _dev(idx, "idx", torch.int32, ni), _stream(stream)), "dllm_select_groups")
 
 
 def reuse_sparse_attn(p: Problem, q_blk, k_cache, v_cache, idx, out_blk, stream=None) -> None:
