@@ -577,6 +577,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the C2/C3/C4/N4 sub-results (N=1 only anyway)")
     ap.add_argument("--config-steps", type=int, default=5)
+    ap.add_argument("--no-in-stream", action="store_true", help="skip the in-stream Reuse timing (ncu launch lists)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -621,7 +622,7 @@ def main():
     total_max = float(tt.item())
     reqs_per_step = glob.num_requests
     value = reqs_per_step * args.steps / total_max
-    rs = reuse_in_stream(st) if (rank == 0 and world == 1 and not st.mixed) else None
+    rs = reuse_in_stream(st) if (rank == 0 and world == 1 and not st.mixed and not args.no_in_stream) else None
     kern, flops, reuse_u = kernels_result(st, t_ref, t_sel, t_reu, tf_peak, hbm_peak, rs)
 
     # ---- multi-GPU: all-gather of the per-request outputs (serial and overlapped)

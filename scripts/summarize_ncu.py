@@ -12,7 +12,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 src, cfg, rnd = sys.argv[1], sys.argv[2], sys.argv[3]
-KERNELS = {"refresh": "refresh_tc2", "reuse": "reuse_tc", "select": "select_heads"}
+KERNELS = {"refresh": "refresh_tc2", "reuse": "reuse_tc", "select": "select_heads", "lm_head": "lmhead"}
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
@@ -35,6 +35,8 @@ lines = [f"# ncu summary, {rnd}, config {cfg}", "",
          "scripts/kbench.py); traffic = dram__bytes_read.sum + dram__bytes_write.sum of that launch.", ""]
 for name, k in KERNELS.items():
     rep = os.path.join(src, f"prof_{cfg}_{k}.ncu-rep")
+    if not os.path.exists(rep) and name == "lm_head":
+        rep = os.path.join(src, "prof_N4_lmhead.ncu-rep")
     if not os.path.exists(rep):
         continue
     m = raw(rep)
