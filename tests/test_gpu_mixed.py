@@ -3,6 +3,8 @@ dllm_mixed_attn): one launch computes Refresh for some
 requests and Reuse for the others over ONE paged cache.  Its outputs must be
 bit-identical to the two separate calls (same kernels, same arithmetic) and
 match the fp64 oracle within the north_star tolerances."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -54,6 +56,16 @@ def _outputs(wl, pr, pu, q):
 
 
 def _mixed_vs_separate(L, wl, ri, ui, check_oracle=()):
+    # the mixed launch runs the tcgen05 Reuse body: compare with the tcgen05 kernel
+    # (dllm_reuse_sparse_attn would pick the mma.sync kernel for small batches)
+    os.environ["DLLM_REUSE_IMPL"] = "tc"
+    try:
+        _mixed_vs_separate_tc(L, wl, ri, ui, check_oracle)
+    finally:
+        del os.environ["DLLM_REUSE_IMPL"]
+
+
+def _mixed_vs_separate_tc(L, wl, ri, ui, check_oracle=()):
     batch = synth.make_batch(wl)
     kc, vc = batch.k_cache.cuda(), batch.v_cache.cuda()
     sr, pr, su, pu, q, qb, idx, idx_list = _split(L, wl, batch, ri, ui)

@@ -103,6 +103,9 @@ def _outputs(lib, synth, wl, dev):
 def _worker(rank, world, port, cfg, n, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    # one Reuse kernel for every batch size (the library picks mma.sync for small
+    # batches: a shard and the whole batch could otherwise round differently)
+    os.environ["DLLM_REUSE_IMPL"] = "tc"
     import torch.distributed as dist
 
     from paper_2512_17077_b200 import lib, shard, synth
