@@ -224,32 +224,6 @@ int reuse_impl_env() {
   return 2;
 }
 
-// Reuse kernel choice for D = 128: a batch that gives every SM less than
-// kSmallReuseKeysPerSm keys runs on the persistent mma.sync kernel (reuse_ws),
-// whose shorter per-unit pipeline wins there; larger batches run on tcgen05.
-// Measured (profiles/r02_ab_reuse_ws_tc.log, one box): C1 (~970 keys per SM) ws
-// 31.7 vs tc 33.8 us; C2 (~2,640) 60.4 vs 60.4; C3 583.8 vs 544.8; C4 550.9 vs 410.6.
-constexpr int64_t kSmallReuseKeysPerSm = 1536;
-int num_sms_api() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
-bool reuse_small_batch(const dllm_problem *p, const Layout &lay, int b0, int b1) {
-  if (getenv("DLLM_REUSE_IMPL")) return false;   // explicit A/B choice wins
-  int64_t keys = 0;
-  for (int b = b0; b < b1; ++b) {
-    const int blk = p->blk_end[b] - p->blk_start[b];
-    keys += (int64_t)p->num_heads * ((blk + 31) / 32) * (blk + lay.k[b]);
-  }
-  return keys < kSmallReuseKeysPerSm * num_sms_api();
-}
-
 int refresh_impl_env() {
   // DLLM_REFRESH_IMPL=mma selects the mma.sync kernel (A/B comparisons); default:
   // tcgen05 (D = 64, 128), else the mma.sync kernel.
@@ -428,8 +402,7 @@ int dllm_reuse_sparse_attn(const dllm_problem *p, const void *q_blk, const void 
       const int blk = p->blk_end[b] - p->blk_start[b];
       return p->num_heads * ((blk + 31) / 32);
     });
-    int impl = reuse_impl_env();
-    if (impl == 2 && reuse_small_batch(p, lay, b0, b1)) impl = 1;
+    const int impl = reuse_impl_env();
     cudaError_t e = impl == 2 && reuse_tc_supported(p->head_dim)
                         ? launch_reuse_tc(pl, q_blk, k_cache, v_cache, idx, out_blk, p->workspace, (cudaStream_t)stream)
                         : launch_reuse_ws(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream);

@@ -48,8 +48,21 @@ namespace rtc {
 
 constexpr int kTD = 128;            // head dim supported by this kernel
 constexpr int kTRows = 32;          // query rows per unit (MMA N)
-constexpr int kTChunk = 128;        // keys per ring stage (MMA M of S^T)
-constexpr int kTNS = 3;             // K/V ring stages (64 KB each; 4 do not fit beside Q and staging)
+#ifndef DLLM_RTC_KEYS
+#define DLLM_RTC_KEYS 96
+#endif
+// Keys per ring stage.  S^T is always an M = 128 MMA (the accumulator layout with
+// one key per TMEM lane); with 96-key stages it reads 32 rows past the stage's K
+// tile (the tile's second atom, then the stage's V tile: finite data) into TMEM
+// lanes 96-127, which the softmax masks.  96-key stages fit 4 deep in the same
+// 192 KB as 3 of 128 keys and waste less of the ring on a unit's partial last
+// stage (C1: 280 keys = 3 x 96 (97% full) vs 2 x 128 + 24 (73%)).  Measured
+// (profiles/r02_ab_reuse_keys96.log, two alternating runs on one box): C1 31.7 vs
+// 33.8 us, C2 56.3 / 62.4 vs 56.3 / 56.3, C3 588 / 547 vs 542 / 555, C4 400 / 396 vs
+// 401 / 410 us (96 vs 128).
+constexpr int kTChunk = DLLM_RTC_KEYS;
+constexpr int kTNS = kTChunk == 128 ? 3 : 4;     // K/V ring stages (2 x kTChunk x 256 B each)
+static_assert(kTChunk % 32 == 0 && kTChunk <= 128, "reuse_tc: stage keys");
 constexpr int kTNT = 4;             // translation ring depth (chunks)
 constexpr int kTTG = 4;             // chunks translated per batch (2 vs 4: within box noise)
 // Warp roles (16 warps; the warp schedulers favour the highest warp id among the
@@ -62,7 +75,7 @@ __device__ __forceinline__ int loader_index(int w) { return w < 4 ? w : (w == 6 
 constexpr int kTThreads = kTWarps * 32;
 
 // shared memory (offsets from a 1024-byte aligned base)
-constexpr int kTileK = kTChunk * kTD * 2;       // 32 KB: [2 atoms][128 rows][128 B]
+constexpr int kTileK = kTChunk * kTD * 2;       // [2 atoms][kTChunk rows][128 B]
 constexpr int kStage = 2 * kTileK;              // K then V
 constexpr int kQTile = kTRows * kTD * 2;        // 8 KB: [2 atoms][32 rows][128 B]
 constexpr int kOffQ = kTNS * kStage;
@@ -482,7 +495,7 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
         ptx::tc_fence_after();
         if (sw == 0) RTC_CHUNK(3, t);
         const int key = c * kTChunk + sw * 32 + lane;
-        const bool valid = key < u.nk;
+        const bool valid = sw * 32 + lane < kTChunk && key < u.nk;   // lanes past the stage: masked
         float x[32];
         float dmax = -INFINITY;
         {
