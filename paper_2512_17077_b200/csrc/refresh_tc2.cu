@@ -68,76 +68,32 @@ namespace {
 
 constexpr int TBM = 128;            // query rows per tile
 constexpr int TBN = 64;             // keys per step
-#ifndef DLLM_TC2_NST
-#define DLLM_TC2_NST 4
-#endif
-constexpr int NST = DLLM_TC2_NST;   // K and V ring stages
+constexpr int NST = 4;              // K and V ring stages (3 measured 7% slower at C1, r01_ab_tc2_nst.log)
 constexpr int THREADS = 512;
-#ifndef DLLM_TC2_RESCALE
-#define DLLM_TC2_RESCALE 8
-#endif
-constexpr float kRescaleLog2 = (float)DLLM_TC2_RESCALE;   // lazy-rescale threshold (log2 units)
-#ifndef DLLM_TC2_PREFETCH
-#define DLLM_TC2_PREFETCH 0
-#endif
-constexpr bool kL2Prefetch = DLLM_TC2_PREFETCH > 0;
-constexpr int kPrefetchSteps = DLLM_TC2_PREFETCH;   // next-unit K/V steps warmed in L2
-#ifndef DLLM_TC2_LAYOUT
-#define DLLM_TC2_LAYOUT 0   // warp-role placement (see the role dispatch; 1 measured neutral)
-#endif
-#ifndef DLLM_TC2_FASTDECODE
-#define DLLM_TC2_FASTDECODE 0   // request cursor + fp32-assisted division in decode_unit (measured 0.5-1% slower)
-#endif
-#ifndef DLLM_TC2_NEXTDECODE
-#define DLLM_TC2_NEXTDECODE 0
-#endif
-constexpr bool kNextDecode = DLLM_TC2_NEXTDECODE;  // decode the next unit mid-unit (producer / MMA / Q warps)
-#ifndef DLLM_TC2_KVMERGED
-#define DLLM_TC2_KVMERGED 0
-#endif
-// one barrier pair per K/V stage (K and V of a step land together, the stage is
-// released after the step's P.V): one wait and one commit fewer per step
-constexpr bool kKVMerged = DLLM_TC2_KVMERGED;
-#ifndef DLLM_TC2_POLY
-#define DLLM_TC2_POLY 1   // 1 of 8 (A/B, one run each: 0 / 1 / 2 of 8 -> C1 972 / 1,002 / 973 TFLOP/s; 3 / 4 of 8
-                          // 987 / 935; 1 of 4 / 16, 3 of 16 and a different share per warpgroup all slower)
-#endif
-// of every 8 exponential pairs of the softmax, this many run as a degree-3
-// polynomial on the FMA pipe instead of MUFU ex2 (16/clk/SM, the same rate at
-// which the tensor cores consume S elements at D = 128)
-constexpr int kPolyPairs = DLLM_TC2_POLY;
-#ifndef DLLM_TC2_POLY_PERIOD
-#define DLLM_TC2_POLY_PERIOD 8   // ... of every DLLM_TC2_POLY_PERIOD pairs (power of two <= 32)
-#endif
-constexpr int kPolyPeriod = DLLM_TC2_POLY_PERIOD;
-#ifndef DLLM_TC2_DYNSCHED
-#define DLLM_TC2_DYNSCHED 1
-#endif
+constexpr float kRescaleLog2 = 8.f; // lazy-rescale threshold (log2 units)
+// of every kPolyPeriod exponential pairs of the softmax, kPolyPairs run as a
+// degree-3 polynomial on the FMA pipe instead of MUFU ex2 (16/clk/SM, the same
+// rate at which the tensor cores consume S elements at D = 128).  Swept in round 1
+// (r01_ab_tc2_poly_sweep.log): 0 / 1 / 2 / 3 / 4 of 8 -> C1 972 / 1,002 / 973 /
+// 987 / 935 TFLOP/s; 1 of 4 / 16, 3 of 16 and per-warpgroup shares all slower.
+constexpr int kPolyPairs = 1;
+constexpr int kPolyPeriod = 8;
 // Dynamic unit scheduling: after its first (static) unit, a CTA claims the next
-// work unit from a device counter when its K/V producer needs it and publishes
-// the id to the other roles through a shared-memory ring, so CTAs that run
-// faster (fewer importance-epilogue units, less contended SMs) take more units.
-constexpr bool kDynSched = DLLM_TC2_DYNSCHED != 0;
-#ifndef DLLM_TC2_QPREFETCH
-// N > 0: the K/V producer claims the next unit N steps before the current one ends
-// and prefetches its Q tiles into L2, so their TMA load at the unit boundary (issued
-// when this unit's Q buffers drain) hits L2.  (Claiming a whole unit ahead was
-// measured 1-3% slower at C1/C2.)
-#define DLLM_TC2_QPREFETCH 0
-#endif
-constexpr bool kQPrefetch = kDynSched && DLLM_TC2_QPREFETCH != 0;
-constexpr int kQPreSteps = DLLM_TC2_QPREFETCH;
-#ifndef DLLM_TC2_REG_SOFTMAX
+// work unit from a device counter (in the caller's workspace) when its K/V
+// producer needs it and publishes the id to the other roles through a
+// shared-memory ring, so CTAs that run faster (fewer importance-epilogue units,
+// less contended SMs) take more units.
+constexpr bool kDynSched = true;
 // register split (setmaxnreg): 8 softmax warps, 4 epilogue warps, 4 others at 64;
-// 2 * softmax + epilogue <= 448 for 64K registers per SM
+// 2 * softmax + epilogue <= 448 for 64K registers per SM (136/176 vs 144/160 vs
+// 152/144 measured neutral, r01_ab_tc2_regsplit.log)
 #define DLLM_TC2_REG_SOFTMAX 136
 #define DLLM_TC2_REG_EPI 176
-#endif
 static_assert(2 * DLLM_TC2_REG_SOFTMAX + DLLM_TC2_REG_EPI <= 448, "register budget");
-#ifndef DLLM_TC2_MMAPOLL
-#define DLLM_TC2_MMAPOLL 0   // 1: the MMA warp serves the two Q tiles in the order their P becomes ready
-#endif
-constexpr bool kMmaPoll = DLLM_TC2_MMAPOLL != 0;
+// Measured in round 1 and removed: L2 prefetch of the next unit's K/V and Q
+// (slower), next-unit decode mid-unit, one barrier pair per K/V stage, an MMA warp
+// serving the two Q tiles in P-ready order (4-5% slower), a request cursor in
+// decode_unit (0.5-1% slower), other warp-role placements (neutral).
 #ifndef DLLM_TC2_FUSEDSEL
 // 1: pool + TopK fused into the epilogue warpgroup (dllm_refresh_select_attn).  Off by
 // default: measured ~13 us per (b, h) selection at C1 (~25k clk, issue-starved beside
@@ -204,29 +160,16 @@ struct Unit {
 // a / b and a % b for 0 <= a < 2^24, 1 <= b < 2^24: fp32 quotient (off by at most
 // one) and one integer correction -- about a tenth of the latency of the integer
 // division sequence, which sat on the unit-boundary critical path of every role
-__device__ __forceinline__ int fast_divmod(int a, int b, int &rem) {
-  int q = (int)__fdividef((float)a, (float)b);
-  int r = a - q * b;
-  if (r < 0) { --q; r += b; } else if (r >= b) { ++q; r -= b; }
-  rem = r;
-  return q;
-}
 
 // `cur` is the caller's cursor into the request table: every role walks its units
 // in increasing order, so the owning request is found by advancing the cursor
 // (usually 0 or 1 step) instead of a binary search
 __device__ __forceinline__ void decode_unit(const Plan &pl, const ReqInfo *rs, int unit, Unit &u, int &cur) {
-#if DLLM_TC2_FASTDECODE
-  if (cur >= pl.nreq || rs[cur].unit_off > unit) cur = 0;
-  while (cur + 1 < pl.nreq && rs[cur + 1].unit_off <= unit) ++cur;
-  const int lo = cur;
-#else
   int lo = 0, hi = pl.nreq - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (rs[mid].unit_off <= unit) lo = mid; else hi = mid - 1;
   }
-#endif
   const ReqInfo &R = rs[lo];
   u.L = R.L; u.bs = R.bs; u.be = R.be;
   u.q_off = R.q_off; u.bt_row = R.bt_row; u.score_off = R.score_off;
@@ -236,22 +179,13 @@ __device__ __forceinline__ void decode_unit(const Plan &pl, const ReqInfo *rs, i
   const int ntiles = nreg + (extra ? 1 : 0);
   const int npairs = (ntiles + 1) >> 1;
   const int local = unit - R.unit_off;
-#if DLLM_TC2_FASTDECODE
-  int pr_rem;
-  u.h = fast_divmod(local, npairs, pr_rem);
+  u.h = local / npairs;
   // tile pairs are rotated by head: units are dealt to CTAs with a stride of
   // gridDim.x (a multiple of 4 on B200), so without the rotation one CTA in
   // npairs would always get the pair that holds the active block, and with it
   // all of the importance-epilogue work (a 30% longer critical path)
-  int p = pr_rem + u.h;
-  fast_divmod(p, npairs, p);
-  int unused;
-  u.kvh = fast_divmod(u.h, pl.H / pl.H_kv, unused);
-#else
-  u.h = local / npairs;
   const int p = (local - u.h * npairs + u.h) % npairs;
   u.kvh = u.h / (pl.H / pl.H_kv);
-#endif
   u.n = (u.L + TBN - 1) / TBN;
   const int t0 = 2 * p, t1 = 2 * p + 1;
   u.tile1 = t1 < ntiles;
@@ -429,7 +363,7 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
   uint8_t *gb = smem_raw + (sb - raw_u32);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto bar = [&](int i) { return sb + C::kOffBar + 8u * (uint32_t)i; };
-  int dcur = 0, dcur2 = 0;   // request-table cursors of decode_unit (per thread, one role each)
+  int dcur = 0;   // request-table cursor of decode_unit (per thread)
 
 #ifdef DLLM_TRACE
   if (threadIdx.x == 0 && blockIdx.x < 1024) { g_cta2[blockIdx.x][0] = gtimer(); g_cta2[blockIdx.x][2] = 0; }
@@ -469,14 +403,7 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
   // warp 8 TMA producer, warp 9 MMA issuer.  The warp scheduler favours the highest
   // warp id among eligible warps of a sub-partition, so the producer and the MMA
   // issuer are placed above the softmax warps sharing their sub-partitions.
-#if DLLM_TC2_LAYOUT == 0
   constexpr int kProducerWarp = 8, kMmaWarp = 9, kQWarp = 10, kEpi0 = 12;
-#else
-  // the MMA issuer shares sub-partition 1 with softmax warps 1, 5 and epilogue warp
-  // 9; as the highest warp id there it is picked first whenever it is eligible
-  // (with the epilogue warpgroup on top, its unit-boundary work ran issue-starved)
-  constexpr int kProducerWarp = 12, kMmaWarp = 13, kQWarp = 14, kEpi0 = 8;
-#endif
   if (warp == kMmaWarp) {
     ptx::tmem_alloc(bar(B_TMEMSLOT), 512);
     ptx::tmem_relinquish();
@@ -485,7 +412,6 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t *>(gb + C::kOffBar + 8 * B_TMEMSLOT);
-  static_assert(!(kDynSched && (kNextDecode || kL2Prefetch)), "next-unit options assume the static unit order");
   // the device counter lives in the caller's workspace (dllm_problem.workspace):
   // without one the units go round-robin
   const bool dyn = kDynSched && plan.sched != nullptr;
@@ -513,7 +439,6 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
     // the next unit is decoded mid-unit (off the unit-boundary critical path)
     Unit un;
     if (cta < plan.total_units) decode_unit(plan, rs, cta, un, dcur);
-    int nxt_claim = -1;   // kQPrefetch: the next unit, claimed kQPreSteps steps before this one ends
     auto claim = [&]() {
       const int c = ncta + atomicAdd(plan.sched, 1);
       return c < plan.total_units ? c : plan.total_units;
@@ -523,8 +448,7 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
       if (dyn) {
         // this role needs the next unit first: claim it and publish it to the others
         if (lane == 0) {
-          unit = i == 0 ? cta : (nxt_claim >= 0 ? nxt_claim : claim());
-          nxt_claim = -1;
+          unit = i == 0 ? cta : claim();
           unit = unit < plan.total_units ? unit : plan.total_units;
           const int slot = i % kRing;
           ptx::mbar_wait(bar(B_REMPTY + slot), ((i / kRing) & 1) ^ 1);
@@ -534,50 +458,12 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
         unit = __shfl_sync(0xffffffffu, unit, 0);
       }
       if (unit >= plan.total_units) break;
-      if (!kNextDecode) decode_unit(plan, rs, unit, un, dcur);
+      decode_unit(plan, rs, unit, un, dcur);
       const Unit u = un;
       const int32_t *bt = plan.block_table + (int64_t)u.bt_row * plan.pages_per_req;
-      if (kL2Prefetch) {
-        // All CTAs reach their unit boundaries at about the same time, so the next
-        // unit's Q tiles and first K/V steps would be requested by every SM at once;
-        // warm L2 with them now, spread over this unit's duration.
-        const int nu = unit + ncta;
-        if (nu < plan.total_units) {
-          Unit v;
-          decode_unit(plan, rs, nu, v, dcur2);
-          const int ntq = v.tile1 ? 2 : 1;
-          if (lane < ntq * C::kChunks)
-            ptx::tma_prefetch_3d(&tm_q, (lane % C::kChunks) * 64, v.h,
-                                 v.q_off + ((lane / C::kChunks) ? v.origin1 : v.origin0));
-          const int32_t *btn = plan.block_table + (int64_t)v.bt_row * plan.pages_per_req;
-          const int nsteps = min(v.n, kPrefetchSteps);
-          for (int e = lane; e < nsteps * nsub; e += 32) {
-            const int key0 = (e / nsub) * TBN + (e % nsub) * boxrows;
-            if (key0 < v.L) {
-              const int page = __ldg(btn + (key0 >> plan.page_shift));
-              const int slot = key0 & (plan.page_size - 1);
-              for (int c = 0; c < C::kChunks; ++c) {
-                ptx::tma_prefetch_4d(&tm_k, c * 64, slot, v.kvh, page);
-                ptx::tma_prefetch_4d(&tm_v, c * 64, slot, v.kvh, page);
-              }
-            }
-          }
-        }
-        __syncwarp();
-      }
       for (int j = 0; j < u.n; ++j, ++it) {
         const int s = it % NST;
         const uint32_t ph = (it / NST) & 1;
-        if (kQPrefetch && lane == 0 && nxt_claim < 0 && j == (u.n > kQPreSteps ? u.n - kQPreSteps : 0)) {
-          nxt_claim = claim();
-          if (nxt_claim < plan.total_units) {
-            Unit v;
-            decode_unit(plan, rs, nxt_claim, v, dcur2);
-            for (int t = 0; t < (v.tile1 ? 2 : 1); ++t)
-              for (int c = 0; c < C::kChunks; ++c)
-                ptx::tma_prefetch_3d(&tm_q, c * 64, v.h, v.q_off + (t ? v.origin1 : v.origin0));
-          }
-        }
         const int key_end = min(TBN, u.L - j * TBN);      // valid keys in this step
         if (lane == 0) {
           int nvalid = 0;
@@ -586,7 +472,7 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
           TRACE2(24, it);
           ptx::mbar_wait(bar(B_KEMPTY + s), ph ^ 1);
           TRACE2(25, it);
-          ptx::mbar_arrive_expect_tx(bar(B_KFULL + s), kKVMerged ? 2 * bytes : bytes);
+          ptx::mbar_arrive_expect_tx(bar(B_KFULL + s), bytes);
           for (int sbx = 0; sbx < nvalid; ++sbx) {
             const int key0 = j * TBN + sbx * boxrows;
             const int page = __ldg(bt + (key0 >> plan.page_shift));
@@ -595,26 +481,23 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
               ptx::tma_load_4d(sb + C::kOffK + s * C::kKVBytes + c * TBN * 128 + sbx * boxrows * 128, &tm_k,
                                bar(B_KFULL + s), c * 64, slot, u.kvh, page);
           }
-          if (!kKVMerged) {
-            TRACE2(26, it);
-            ptx::mbar_wait(bar(B_VEMPTY + s), ph ^ 1);
-            TRACE2(27, it);
-            ptx::mbar_arrive_expect_tx(bar(B_VFULL + s), bytes);
-          }
+          TRACE2(26, it);
+          ptx::mbar_wait(bar(B_VEMPTY + s), ph ^ 1);
+          TRACE2(27, it);
+          ptx::mbar_arrive_expect_tx(bar(B_VFULL + s), bytes);
           for (int sbx = 0; sbx < nvalid; ++sbx) {
             const int key0 = j * TBN + sbx * boxrows;
             const int page = __ldg(bt + (key0 >> plan.page_shift));
             const int slot = key0 & (plan.page_size - 1);
             for (int c = 0; c < C::kChunks; ++c)
               ptx::tma_load_4d(sb + C::kOffV + s * C::kKVBytes + c * TBN * 128 + sbx * boxrows * 128, &tm_v,
-                               bar((kKVMerged ? B_KFULL : B_VFULL) + s), c * 64, slot, u.kvh, page);
+                               bar(B_VFULL + s), c * 64, slot, u.kvh, page);
           }
         }
         __syncwarp();
-        if (kNextDecode && j == 0 && unit + ncta < plan.total_units) decode_unit(plan, rs, unit + ncta, un, dcur);
         if (key_end < TBN) {
           // zero V rows >= key_end (P is 0 there, but 0 * NaN would poison O)
-          ptx::mbar_wait(bar((kKVMerged ? B_KFULL : B_VFULL) + s), ph);
+          ptx::mbar_wait(bar(B_VFULL + s), ph);
           uint8_t *vbase = gb + C::kOffV + s * C::kKVBytes;
           const int nrow = TBN - key_end;
           for (int e = lane; e < nrow * 8 * C::kChunks; e += 32) {
@@ -641,9 +524,8 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
       for (int i = 0;; ++i, ++ucnt) {
         const int unit = unit_at(i, false);
         if (unit >= plan.total_units) break;
-        if (!kNextDecode) decode_unit(plan, rs, unit, un, dcur);
+        decode_unit(plan, rs, unit, un, dcur);
         const Unit u = un;
-        if (kNextDecode && unit + ncta < plan.total_units) decode_unit(plan, rs, unit + ncta, un, dcur);
         TRACE2(20, ucnt);
         ptx::mbar_wait(bar(B_QEMPTY), (ucnt & 1) ^ 1);
         TRACE2(21, ucnt);
@@ -677,7 +559,7 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
         const int unit = unit_at(i, true);
         if (unit >= plan.total_units) break;
         if (lane == 0) TRACE2(23, 2 * ucnt);
-        if (!kNextDecode) decode_unit(plan, rs, unit, un, dcur);
+        decode_unit(plan, rs, unit, un, dcur);
         const Unit u = un;
         if (lane == 0) TRACE2(23, 2 * ucnt + 1);
         const int nt = u.tile1 ? 2 : 1;
@@ -717,14 +599,13 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
           if (lane == 0) TRACE2(18 + jj, ucnt);
           ptx::tc_fence_after();
           for (int i = 0; i < nt; ++i) qk(i, st);
-          if (!kKVMerged) ptx::mma_commit_elect(bar(B_KEMPTY + st));
+          ptx::mma_commit_elect(bar(B_KEMPTY + st));
         }
         if (u.n <= 2) ptx::mma_commit_elect(bar(B_QEMPTY));
-        if (kNextDecode && unit + ncta < plan.total_units) decode_unit(plan, rs, unit + ncta, un, dcur);
         for (int j = 0; j < u.n; ++j) {
           const int sv = (it + j) % NST;
           if (lane == 0) TRACE2(10, it + j);
-          if (!kKVMerged) ptx::mbar_wait(bar(B_VFULL + sv), ((it + j) / NST) & 1);
+          ptx::mbar_wait(bar(B_VFULL + sv), ((it + j) / NST) & 1);
           if (lane == 0) TRACE2(11, it + j);
           if (j == u.n - 1 && (u.L % TBN) != 0) {
             ptx::mbar_wait(bar(B_VZ), vzc & 1);
@@ -732,7 +613,6 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
           }
           const bool ahead = j + 2 < u.n;
           const int sk = (it + j + 2) % NST;
-          if (!kMmaPoll) {
           for (int i = 0; i < nt; ++i) {
             const int b = gp[i] & 1;
             if (lane == 0) TRACE2(6 + 2 * i, gp[i]);
@@ -755,40 +635,11 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
               qk(i, sk);
             }
           }
-          } else {
-            // whichever tile's P is ready first goes first (the two softmax warpgroups
-            // are not forced into lock-step by the issue order)
-            bool done[2] = {false, nt < 2};
-            bool kready = false;
-            while (!(done[0] && done[1])) {
-#pragma unroll
-              for (int i = 0; i < 2; ++i) {
-                if (done[i]) continue;
-                const int b = gp[i] & 1;
-                bool ready = ptx::mbar_test_wait(bar(B_PFULL + 2 * i + b), (gp[i] >> 1) & 1);
-                if (j == 0) ready = ready && ptx::mbar_test_wait(bar(B_OFREE + i), (ou[i] & 1) ^ 1);
-                ready = __shfl_sync(0xffffffffu, ready, 0);
-                if (!ready) continue;
-                if (j == 0) ++ou[i];
-                ptx::tc_fence_after();
-                pv(i, sv, j > 0, j == u.n - 1);
-                if (ahead) {
-                  if (!kready) {
-                    ptx::mbar_wait(bar(B_KFULL + sk), ((it + j + 2) / NST) & 1);
-                    ptx::tc_fence_after();
-                    kready = true;
-                  }
-                  qk(i, sk);
-                }
-                done[i] = true;
-              }
-            }
-          }
           if (ahead) {
-            if (!kKVMerged) ptx::mma_commit_elect(bar(B_KEMPTY + sk));
+            ptx::mma_commit_elect(bar(B_KEMPTY + sk));
             if (j + 2 == u.n - 1) ptx::mma_commit_elect(bar(B_QEMPTY));
           }
-          ptx::mma_commit_elect(bar((kKVMerged ? B_KEMPTY : B_VEMPTY) + sv));
+          ptx::mma_commit_elect(bar(B_VEMPTY + sv));
           if (lane == 0 && j == u.n - 1) TRACE2(22, ucnt);
         }
         it += u.n;
