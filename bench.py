@@ -345,7 +345,9 @@ class Step:
         for pc, bf in zip(self.pieces, bufs):
             if pc["reuse"]:
                 q, qb, kc, vc = pc["t"]
-                lib.reuse_sparse_attn(pc["p"], qb, kc, vc, bf.idx, bf.out_blk, stream)
+                # one set per KV group: the group kernel gathers each group's rows once
+                (lib.reuse_group_sets if self.select == "groups" else lib.reuse_sparse_attn)(
+                    pc["p"], qb, kc, vc, bf.idx, bf.out_blk, stream)
         rec(3)
 
     def algorithmic(self):
@@ -454,15 +456,17 @@ def reuse_in_stream(st, reps=BLOCK_CYCLE_REUSE, iters=5):
                          pool_window=sub.pool_window, page_size=sub.page_size, block_table=bt.block_table.to(dev))
         bf = lib.alloc_buffers(pp, device=dev)
         kk = pp.layout()[0]
-        flat = np.concatenate([x.reshape(-1) for x in synth.indices(sub, kk)]).astype(np.int32)
+        mode = "shared" if st.select == "groups" else "random"
+        flat = np.concatenate([x.reshape(-1) for x in synth.indices(sub, kk, mode=mode)]).astype(np.int32)
         bf.idx[:flat.size].copy_(torch.from_numpy(flat))
         sets.append((pp, bt.q_blk.to(dev), bt.k_cache.to(dev), bt.v_cache.to(dev), bf))
+    reuse = lib.reuse_group_sets if st.select == "groups" else lib.reuse_sparse_attn
     cs = torch.cuda.Stream(dev)
 
     def launches():
         for i in range(reps):
             pp, qb, kc, vc, bf = sets[i % nsets]
-            lib.reuse_sparse_attn(pp, qb, kc, vc, bf.idx, bf.out_blk, cs)
+            reuse(pp, qb, kc, vc, bf.idx, bf.out_blk, cs)
 
     cs.wait_stream(torch.cuda.current_stream(dev))
     with torch.cuda.stream(cs):
@@ -560,7 +564,8 @@ def config_result(cfg_name, dev, lib, synth, shard, tf_peak, hbm_peak, steps, wa
     kern, flops, reuse_u = kernels_result(st, t_ref, t_sel, t_reu, tf_peak, hbm_peak, rs)
     del g
     return {"workload": workload_desc(wl, 1, "weak") + ("" if select == "heads" else
-                                                       ", selection: one set per KV group (dllm_select_groups)"),
+                                                       ", selection: one set per KV group (dllm_select_groups),"
+                                                       " Reuse dllm_reuse_group_sets"),
             "requests_per_s": wl.num_requests * steps / total,
             "ms_per_step": 1e3 * total / steps, "launch_mode": "cuda_graph", "kernels": kern}
 

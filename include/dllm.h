@@ -179,6 +179,18 @@ DLLM_API int dllm_reuse_sparse_attn(const dllm_problem *p, const void *q_blk, co
                            const void *v_cache, const int32_t *idx, void *out_blk,
                            void *stream);
 
+/* Reuse over per-KV-group sets (next row N2, GQA; R21): the same
+ * result as dllm_reuse_sparse_attn (Eq. 4) when every head of
+ * a KV group holds the same index list, as dllm_select_groups writes them.
+ * Precondition (not checked): for every request b and KV head g, idx(b, h) is
+ * equal for all h with kv(h) = g; only the list of the group's first head of
+ * each run of up to 4 heads is read.  The group's K/V rows are gathered once
+ * for up to 4 of its heads instead of once per head.  Same layouts, pointers
+ * and errors as dllm_reuse_sparse_attn, to which it falls back when H = H_kv
+ * or D != 128.  All DEVICE. */
+DLLM_API int dllm_reuse_group_sets(const dllm_problem *p, const void *q_blk, const void *k_cache,
+                                   const void *v_cache, const int32_t *idx, void *out_blk, void *stream);
+
 /* Pack (the paper's physical layout, §4.5: "pack the sparse
  * tokens into a physically dense KV layout", [N_heads, rL, D_head]): for every
  * (b, h, i), k_pack[(H*cu_k[b] + h*k_b + i) * D + d] = K[idx(b,h,i), kv(h), d]

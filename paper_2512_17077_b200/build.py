@@ -24,7 +24,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(HERE, "..", "include")]
-SOURCES = ["dllm_api.cu", "select.cu", "reuse_ws.cu", "reuse_tc.cu", "lmhead.cu", "refresh_mma.cu", "refresh_tc2.cu"]
+SOURCES = ["dllm_api.cu", "select.cu", "reuse_ws.cu", "reuse_tc.cu", "reuse_grp.cu", "lmhead.cu", "refresh_mma.cu", "refresh_tc2.cu"]
 
 
 def _compile(src: str, verbose: bool) -> str:

@@ -49,6 +49,10 @@ int refresh_tc2_units(int L, int bs, int be, int H, bool with_scores);
 cudaError_t launch_refresh_tc2(const Plan &, const void *, const void *, const void *, void *, float *, int32_t *,
                                void *, cudaStream_t);
 int fused_select_max_n();
+int reuse_grp_units(int H, int H_kv, int blk);
+bool reuse_grp_supported(int D);
+cudaError_t launch_reuse_grp(const Plan &, const void *, const void *, const void *, const int32_t *, void *,
+                             cudaStream_t);
 }  // namespace dllm
 
 using namespace dllm;
@@ -407,6 +411,34 @@ int dllm_reuse_sparse_attn(const dllm_problem *p, const void *q_blk, const void 
                         ? launch_reuse_tc(pl, q_blk, k_cache, v_cache, idx, out_blk, p->workspace, (cudaStream_t)stream)
                         : launch_reuse_ws(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "reuse launch");
+  }
+  return ok();
+}
+
+int dllm_reuse_group_sets(const dllm_problem *p, const void *q_blk, const void *k_cache, const void *v_cache,
+                          const int32_t *idx, void *out_blk, void *stream) {
+  Layout lay;
+  int st = make_layout(p, lay);
+  if (st) return st;
+  const int B = p->num_requests;
+  if (B == 0) return ok();
+  // one set per KV group is a special case of per-head sets: the per-head kernel
+  // computes the same attention (head dims the group kernel does not cover,
+  // MHA where a group is one head, and the A/B switch DLLM_REUSE_IMPL=ws)
+  if (!reuse_grp_supported(p->head_dim) || p->num_heads == p->num_kv_heads || reuse_impl_env() != 2)
+    return dllm_reuse_sparse_attn(p, q_blk, k_cache, v_cache, idx, out_blk, stream);
+  if (!q_blk || !k_cache || !v_cache || !out_blk) return fail(DLLM_ERR_INVALID_ARG, "reuse_group_sets: NULL tensor pointer");
+  if (!idx && lay.cu_k[B] > 0) return fail(DLLM_ERR_INVALID_ARG, "reuse_group_sets: idx is NULL");
+  if (!aligned16(q_blk) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out_blk))
+    return fail(DLLM_ERR_SHAPE, "reuse_group_sets: bf16 tensors must be 16-byte aligned");
+  static thread_local Plan pl;
+  for (int b0 = 0; b0 < B; b0 += kMaxReqPerLaunch) {
+    const int b1 = b0 + kMaxReqPerLaunch < B ? b0 + kMaxReqPerLaunch : B;
+    fill_plan(pl, p, lay.k, b0, b1, lay.cu_L, lay.cu_blk, lay.cu_k, [&](int b) {
+      return reuse_grp_units(p->num_heads, p->num_kv_heads, p->blk_end[b] - p->blk_start[b]);
+    });
+    cudaError_t e = launch_reuse_grp(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "reuse_group_sets launch");
   }
   return ok();
 }

@@ -29,7 +29,7 @@ DLLM_ERR_CUDA = -5
 EXPORTED = ("dllm_workspace_bytes", "dllm_keep_count", "dllm_index_layout", "dllm_refresh_attn", "dllm_select_heads",
             "dllm_select_global", "dllm_select_groups",
             "dllm_refresh_select_attn", "dllm_mixed_select_attn",
-            "dllm_reuse_sparse_attn", "dllm_pack_kv", "dllm_reuse_packed", "dllm_mixed_attn", "dllm_logit_chunks",
+            "dllm_reuse_sparse_attn", "dllm_reuse_group_sets", "dllm_pack_kv", "dllm_reuse_packed", "dllm_mixed_attn", "dllm_logit_chunks",
             "dllm_lm_head_workspace_bytes", "dllm_lm_head_argmax", "dllm_check_indices", "dllm_status_string",
             "dllm_last_error", "dllm_version")
 
@@ -86,6 +86,8 @@ def _load() -> ctypes.CDLL:
         lib.dllm_select_groups.restype = ctypes.c_int
     lib.dllm_reuse_sparse_attn.argtypes = [P, vp, vp, vp, vp, vp, vp]
     lib.dllm_reuse_sparse_attn.restype = ctypes.c_int
+    lib.dllm_reuse_group_sets.argtypes = [P, vp, vp, vp, vp, vp, vp]
+    lib.dllm_reuse_group_sets.restype = ctypes.c_int
     lib.dllm_pack_kv.argtypes = [P, vp, vp, vp, vp, vp, vp]
     lib.dllm_pack_kv.restype = ctypes.c_int
     lib.dllm_reuse_packed.argtypes = [P, vp, vp, vp, vp, vp, vp, vp]
@@ -309,6 +311,15 @@ def reuse_sparse_attn(p: Problem, q_blk, k_cache, v_cache, idx, out_blk, stream=
     _check(_lib.dllm_reuse_sparse_attn(p.ref, _dev(q_blk, "q_blk", bf, nb), _dev(k_cache, "k_cache", bf),
                                        _dev(v_cache, "v_cache", bf), _dev(idx, "idx", torch.int32, ni),
                                        _dev(out_blk, "out_blk", bf, nb), _stream(stream)), "dllm_reuse_sparse_attn")
+
+
+def reuse_group_sets(p: Problem, q_blk, k_cache, v_cache, idx, out_blk, stream=None) -> None:
+    """dllm_reuse_group_sets (Eq. 4 over one key set per KV group, as select_groups writes them)."""
+    bf = torch.bfloat16
+    _, _, ni, nb = _sizes(p)
+    _check(_lib.dllm_reuse_group_sets(p.ref, _dev(q_blk, "q_blk", bf, nb), _dev(k_cache, "k_cache", bf),
+                                      _dev(v_cache, "v_cache", bf), _dev(idx, "idx", torch.int32, ni),
+                                      _dev(out_blk, "out_blk", bf, nb), _stream(stream)), "dllm_reuse_group_sets")
 
 
 def pack_kv(p: Problem, k_cache, v_cache, idx, k_pack, v_pack, stream=None) -> None:

@@ -42,17 +42,17 @@ def main():
     p = lib.Problem(wl.seq_len, wl.blk_start, wl.blk_end, num_heads=wl.num_heads, num_kv_heads=wl.num_kv_heads,
                     head_dim=wl.head_dim, keep_ratio=wl.keep_ratio, pool_window=wl.pool_window,
                     page_size=wl.page_size, block_table=bt)
-    p_nows = lib.Problem(wl.seq_len, wl.blk_start, wl.blk_end, num_heads=wl.num_heads, num_kv_heads=wl.num_kv_heads,
-                         head_dim=wl.head_dim, keep_ratio=wl.keep_ratio, pool_window=wl.pool_window,
-                         page_size=wl.page_size, block_table=bt, workspace=None)
     q, qb, kc, vc = batch.q.cuda(), batch.q_blk.cuda(), batch.k_cache.cuda(), batch.v_cache.cuda()
     buf = lib.alloc_buffers(p)
+    gidx = torch.empty_like(buf.idx)   # one set per KV group (select_groups), for the group kernel
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     fns = {
         "refresh": lambda: lib.refresh_attn(p, q, kc, vc, buf.out, buf.scores),
         "select": lambda: lib.select_heads(p, buf.scores, buf.idx),
         "reuse": lambda: lib.reuse_sparse_attn(p, qb, kc, vc, buf.idx, buf.out_blk),
-        "reuse_nows": lambda: lib.reuse_sparse_attn(p_nows, qb, kc, vc, buf.idx, buf.out_blk),
+        "select_groups": lambda: lib.select_groups(p, buf.scores, gidx),
+        "reuse_group_sets": lambda: lib.reuse_group_sets(p, qb, kc, vc, gidx, buf.out_blk),
+        "reuse_per_head_on_group_sets": lambda: lib.reuse_sparse_attn(p, qb, kc, vc, gidx, buf.out_blk),
         "refresh_select": lambda: lib.refresh_select_attn(p, q, kc, vc, buf.out, buf.scores, buf.idx),
     }
     k_, total_idx_, _, _ = p.layout()
@@ -89,8 +89,13 @@ def main():
     t = res["reuse"][0]
     print(f"{args.cfg} reuse  : {t*1e6:.1f} us  {ub/t/1e9:.1f} GB/s unique ({lb/t/1e9:.1f} logical), "
           f"unique {ub/1e6:.1f} MB")
-    t = res["reuse_nows"][0]
-    print(f"{args.cfg} reuse (no workspace: whole units): {t*1e6:.1f} us  {ub/t/1e9:.1f} GB/s unique")
+    gub, glb = reuse_unique_bytes(wl, k, gidx.cpu().numpy()[:total_idx])
+    t = res["select_groups"][0]
+    print(f"{args.cfg} select_groups: {t*1e6:.1f} us")
+    for name in ("reuse_group_sets", "reuse_per_head_on_group_sets"):
+        t = res[name][0]
+        print(f"{args.cfg} {name}: {t*1e6:.1f} us  {gub/t/1e9:.1f} GB/s unique ({glb/t/1e9:.1f} logical), "
+              f"unique {gub/1e6:.1f} MB (min {res[name][1]*1e6:.1f})")
     t = res["pack"][0]
     pb = 2 * 2 * total_idx * wl.head_dim * 2
     print(f"{args.cfg} pack   : {t*1e6:.1f} us  {pb/t/1e9:.1f} GB/s (read+write {pb/1e6:.1f} MB)")
