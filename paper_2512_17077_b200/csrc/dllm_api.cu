@@ -52,7 +52,10 @@ int fused_select_max_n();
 int reuse_grp_units(int H, int H_kv, int blk);
 bool reuse_grp_supported(int D);
 cudaError_t launch_reuse_grp(const Plan &, const void *, const void *, const void *, const int32_t *, void *,
-                             cudaStream_t);
+                             bool union_sets, cudaStream_t);
+int reuse_union_max_len();
+// union mode needs a KV group of at least 2 query heads
+constexpr int kUnionMinGroup = 2;
 }  // namespace dllm
 
 using namespace dllm;
@@ -220,12 +223,18 @@ int cuda_fail(cudaError_t e, const char *what) {
   return fail(DLLM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+// Reuse kernel choice: 1 = persistent mma.sync (DLLM_REUSE_IMPL=ws), 2 = tcgen05 per
+// head (=tc), 3 = tcgen05 over the union of up to 4 heads' sets of a KV group
+// (=union, GQA, L <= 8192: one gather per sub-group, each head masked to its own
+// keys; it pays only when the heads' sets overlap strongly -- on the synthetic C2
+// selections 74.6 vs 56.3 us, profiles/r02_ab_reuse_union.log); default 0: per head
+// (D = 128), else mma.sync.
 int reuse_impl_env() {
-  // DLLM_REUSE_IMPL=ws selects the persistent mma.sync kernel (A/B comparisons);
-  // default: tcgen05 (D = 128), else the persistent mma.sync kernel.
   const char *s = getenv("DLLM_REUSE_IMPL");
   if (s && !strcmp(s, "ws")) return 1;
-  return 2;
+  if (s && !strcmp(s, "tc")) return 2;
+  if (s && !strcmp(s, "union")) return 3;
+  return 0;
 }
 
 int refresh_impl_env() {
@@ -400,16 +409,22 @@ int dllm_reuse_sparse_attn(const dllm_problem *p, const void *q_blk, const void 
   if (!aligned16(q_blk) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out_blk))
     return fail(DLLM_ERR_SHAPE, "reuse: bf16 tensors must be 16-byte aligned");
   static thread_local Plan pl;
+  const int impl = reuse_impl_env();
   for (int b0 = 0; b0 < B; b0 += kMaxReqPerLaunch) {
     const int b1 = b0 + kMaxReqPerLaunch < B ? b0 + kMaxReqPerLaunch : B;
+    int max_len = 0;
+    for (int b = b0; b < b1; ++b) max_len = p->seq_len[b] > max_len ? p->seq_len[b] : max_len;
+    const bool use_union = impl == 3 && p->num_heads / p->num_kv_heads >= kUnionMinGroup &&
+                           reuse_grp_supported(p->head_dim) && max_len <= reuse_union_max_len();
     fill_plan(pl, p, lay.k, b0, b1, lay.cu_L, lay.cu_blk, lay.cu_k, [&](int b) {
       const int blk = p->blk_end[b] - p->blk_start[b];
-      return p->num_heads * ((blk + 31) / 32);
+      return use_union ? reuse_grp_units(p->num_heads, p->num_kv_heads, blk) : p->num_heads * ((blk + 31) / 32);
     });
-    const int impl = reuse_impl_env();
-    cudaError_t e = impl == 2 && reuse_tc_supported(p->head_dim)
-                        ? launch_reuse_tc(pl, q_blk, k_cache, v_cache, idx, out_blk, p->workspace, (cudaStream_t)stream)
-                        : launch_reuse_ws(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream);
+    cudaError_t e = use_union
+        ? launch_reuse_grp(pl, q_blk, k_cache, v_cache, idx, out_blk, true, (cudaStream_t)stream)
+        : impl != 1 && reuse_tc_supported(p->head_dim)
+              ? launch_reuse_tc(pl, q_blk, k_cache, v_cache, idx, out_blk, p->workspace, (cudaStream_t)stream)
+              : launch_reuse_ws(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "reuse launch");
   }
   return ok();
@@ -425,7 +440,7 @@ int dllm_reuse_group_sets(const dllm_problem *p, const void *q_blk, const void *
   // one set per KV group is a special case of per-head sets: the per-head kernel
   // computes the same attention (head dims the group kernel does not cover,
   // MHA where a group is one head, and the A/B switch DLLM_REUSE_IMPL=ws)
-  if (!reuse_grp_supported(p->head_dim) || p->num_heads == p->num_kv_heads || reuse_impl_env() != 2)
+  if (!reuse_grp_supported(p->head_dim) || p->num_heads == p->num_kv_heads || reuse_impl_env() == 1)
     return dllm_reuse_sparse_attn(p, q_blk, k_cache, v_cache, idx, out_blk, stream);
   if (!q_blk || !k_cache || !v_cache || !out_blk) return fail(DLLM_ERR_INVALID_ARG, "reuse_group_sets: NULL tensor pointer");
   if (!idx && lay.cu_k[B] > 0) return fail(DLLM_ERR_INVALID_ARG, "reuse_group_sets: idx is NULL");
@@ -437,7 +452,7 @@ int dllm_reuse_group_sets(const dllm_problem *p, const void *q_blk, const void *
     fill_plan(pl, p, lay.k, b0, b1, lay.cu_L, lay.cu_blk, lay.cu_k, [&](int b) {
       return reuse_grp_units(p->num_heads, p->num_kv_heads, p->blk_end[b] - p->blk_start[b]);
     });
-    cudaError_t e = launch_reuse_grp(pl, q_blk, k_cache, v_cache, idx, out_blk, (cudaStream_t)stream);
+    cudaError_t e = launch_reuse_grp(pl, q_blk, k_cache, v_cache, idx, out_blk, false, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "reuse_group_sets launch");
   }
   return ok();
@@ -528,7 +543,7 @@ int mixed_impl(const dllm_problem *p_refresh, const void *q, void *out, float *s
        p_refresh->head_dim != p_reuse->head_dim || p_refresh->page_size != p_reuse->page_size))
     return fail(DLLM_ERR_SHAPE, "mixed: the two problems address one paged cache and must agree on H, H_kv, D, page");
   const bool single = Br > 0 && Bu > 0 && Br <= kMaxReqPerLaunch && Bu <= kMaxReqPerLaunch &&
-                      p_refresh->head_dim == 128 && refresh_impl_env() == 2 && reuse_impl_env() == 2;
+                      p_refresh->head_dim == 128 && refresh_impl_env() == 2 && reuse_impl_env() != 1;
   if (!single) {
     // not expressible as one launch (a phase is empty, > kMaxReqPerLaunch requests, or
     // a head dim / A-B override outside the two tcgen05 kernels): the same work as

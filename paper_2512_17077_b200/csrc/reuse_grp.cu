@@ -60,9 +60,22 @@ constexpr int kQTile = kN * kD * 2;                 // 32 KB: [2 atoms][128 rows
 constexpr int kOffQ = kNS * kStage;
 constexpr int kOffOffs = kOffQ + 2 * kQTile;        // [kNT][kChunk] int32
 constexpr int kOffL = kOffOffs + kNT * kChunk * 4;  // [2 O buffers][128 rows] row sums
-constexpr int kBtMax = 1024;                        // block-table entries cached in shared memory
+constexpr int kBtMax = 512;                         // block-table entries cached in shared memory
 constexpr int kOffBt = kOffL + 2 * kN * 4;
-constexpr int kOffBar = kOffBt + kBtMax * 4;
+// union mode (per-head sets): per-head position bitmaps of the unit, their union's
+// word prefix counts, per-chunk head-membership masks and per-unit key counts
+constexpr int kWMax = 256;                          // bitmap words: L <= 8192
+constexpr int kMaxUnionLen = 32 * kWMax;
+constexpr int kRing = 16;                           // > chunks the translator runs ahead of the softmax
+constexpr int kOffBm = kOffBt + kBtMax * 4;         // [kGH][kWMax] u32
+// union keys staged in ascending order (position | membership << 24): a batch of
+// kTG chunks plus one 1024-position scan step (one bitmap word per lane)
+constexpr int kStageKeys = 2048;
+static_assert(kStageKeys >= kTG * kChunk + 1024 && (kStageKeys & (kStageKeys - 1)) == 0, "union staging ring");
+constexpr int kOffStageK = kOffBm + kGH * kWMax * 4;   // [kStageKeys] int32
+constexpr int kOffMask = kOffStageK + kStageKeys * 4;  // [kRing][kGH][kChunk / 32] u32
+constexpr int kOffNk = kOffMask + kRing * kGH * (kChunk / 32) * 4;   // [kRing] int32
+constexpr int kOffBar = kOffNk + kRing * 4;
 constexpr int kNumBars = 2 * kNS + 2 * kNT + 2 * 7 + 1 + 1;
 constexpr int kBytes = kOffBar + 8 * kNumBars + 1024;   // + alignment slack
 static_assert(kBytes <= 227 * 1024, "reuse_grp shared memory");
@@ -102,7 +115,7 @@ __device__ __forceinline__ long long rgs_timer() {
 #endif
 
 struct GUnit {
-  int b, kvh, h0, nh, rg, blk, bs, nk, blk_off, bt_row;
+  int b, kvh, h0, nh, rg, blk, bs, nk, L, k, blk_off, bt_row;
   int64_t idx_off;
 };
 
@@ -124,12 +137,15 @@ __device__ __forceinline__ void gdecode(const Plan &pl, int unit, GUnit &u) {
   u.kvh = local / ngroups;
   u.h0 = u.kvh * G + sg * kGH;
   u.nh = min(kGH, G - sg * kGH);
-  u.nk = u.blk + R.k;
+  u.nk = u.blk + R.k;   // group sets; union mode: blk + |union|, counted by the translator
+  u.L = R.L;
+  u.k = R.k;
   u.blk_off = R.blk_off;
   u.bt_row = R.bt_row;
   u.idx_off = R.idx_off + (int64_t)u.h0 * R.k;   // the group's set, read from the sub-group's first head
 }
 
+template <bool kUnion>
 __global__ void __launch_bounds__(kThreads, 1)
 reuse_grp_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restrict__ q_blk,
                  const __nv_bfloat16 *__restrict__ k_cache, const __nv_bfloat16 *__restrict__ v_cache,
@@ -168,7 +184,7 @@ reuse_grp_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restr
 #endif
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
-      ptx::mbar_init(b_kvfull + 8 * i, 32 * kLoaders);
+      ptx::mbar_init(b_kvfull + 8 * i, 32 * kLoaders + 1);   // + loader 0's release of the translator's data
       ptx::mbar_init(b_kvempty + 8 * i, 1);
     }
     for (int i = 0; i < kNT; ++i) {
@@ -198,6 +214,7 @@ reuse_grp_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restr
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t *>(gb + (b_tslot - sb));
 
+  // (setmaxnreg acts per warpgroup: every warp of a warpgroup requests the same count)
   if (warp < kSoft0) asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n" ::: "memory");
   if (warp == kTransWarp) {
     // ============================ translator ============================
@@ -210,15 +227,129 @@ reuse_grp_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restr
       gdecode(plan, unit, u);
       const int32_t *my_idx = idx + u.idx_off;
       const int32_t *bt = plan.block_table + (int64_t)u.bt_row * plan.pages_per_req;
+      const int W = (u.L + 31) >> 5;
+      const uint32_t *bm = reinterpret_cast<const uint32_t *>(gb + kOffBm);
+      int *stage = reinterpret_cast<int *>(gb + kOffStageK);
+      int staged = 0, scan_pos = 0, n_union = 0;
+      if constexpr (kUnion) {
+        // the sub-group's sets as position bitmaps (heads h0.. are consecutive in idx:
+        // one contiguous list of nh * k entries), then the size of their union
+        uint32_t *bmw = reinterpret_cast<uint32_t *>(gb + kOffBm);
+        for (int j = 0; j < u.nh; ++j)
+          for (int w = lane; w < W; w += 32) bmw[j * kWMax + w] = 0u;
+        __syncwarp();
+        const int total = u.nh * u.k;
+        {
+          // the next unit's lists go to L2 while this one is built and translated
+          const int nu = unit_at(i + 1);
+          if (nu < plan.total_units && lane == 0) {
+            GUnit v;
+            gdecode(plan, nu, v);
+            if (v.k > 0) {
+              const uintptr_t a0 = reinterpret_cast<uintptr_t>(idx + v.idx_off) & ~uintptr_t(15);
+              const uintptr_t a1 =
+                  (reinterpret_cast<uintptr_t>(idx + v.idx_off + (int64_t)v.nh * v.k) + 15) & ~uintptr_t(15);
+              ptx::bulk_prefetch_l2(reinterpret_cast<const void *>(a0), (uint32_t)(a1 - a0));
+            }
+          }
+        }
+        for (int e0 = 0; e0 < total; e0 += 16 * 32) {
+          int pv[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int e = e0 + q * 32 + lane;
+            pv[q] = e < total ? __ldg(my_idx + e) : -1;
+          }
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int e = e0 + q * 32 + lane;
+            const int j = (e >= u.k) + (e >= 2 * u.k) + (e >= 3 * u.k);
+            if (pv[q] >= 0) atomicOr(bmw + j * kWMax + (pv[q] >> 5), 1u << (pv[q] & 31));
+          }
+        }
+        __syncwarp();
+        int cnt = 0;
+        for (int w = lane; w < W; w += 32) {
+          uint32_t uw = 0;
+          for (int j = 0; j < u.nh; ++j) uw |= bm[j * kWMax + w];
+          cnt += __popc(uw);
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        n_union = cnt;
+        u.nk = u.blk + n_union;
+        if (lane == 0) reinterpret_cast<int *>(gb + kOffNk)[i % kRing] = u.nk;
+        RGS_CHUNK(12, i);
+        __syncwarp();
+      }
       const int nchunks = (u.nk + kChunk - 1) / kChunk;
       const bool bt_smem = plan.pages_per_req <= kBtMax;
       for (int g0 = 0; g0 < nchunks; g0 += kTG) {
         constexpr int Q = kTG * kChunk / 32;
         int pos[Q], off[Q];
+        uint32_t memb[Q];
+        if constexpr (kUnion) {
+          // stream the union in ascending position order into the staging ring until
+          // it holds every union key of this batch: 128 positions per step, lane l
+          // owning positions scan_pos + 4 l .. + 3 (membership nibbles from the
+          // bitmaps, a warp prefix sum for the output slots)
+          const int need = min((g0 + kTG) * kChunk - u.blk, n_union);
+          while (staged < need) {
+            // one bitmap word (32 positions) per lane; the lanes' output offsets are a
+            // prefix sum of their counts, formed from ballots of the count bits (no
+            // shuffle chain: the translator shares the MIO pipe with the gathers)
+            const int w = scan_pos + lane;
+            uint32_t bw[kGH], un = 0;
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          const int j = g0 * kChunk + q * 32 + lane;
-          pos[q] = j < u.nk ? (j < u.blk ? u.bs + j : __ldg(my_idx + (j - u.blk))) : -1;
+            for (int j = 0; j < kGH; ++j) {
+              bw[j] = (j < u.nh && w < W) ? bm[j * kWMax + w] : 0u;
+              un |= bw[j];
+            }
+            const int n = __popc(un);
+            const uint32_t lt = (1u << lane) - 1u;
+            int before = 0, tot = 0;
+#pragma unroll
+            for (int bit = 0; bit < 6; ++bit) {
+              const uint32_t bal = __ballot_sync(0xffffffffu, (n >> bit) & 1);
+              before += __popc(bal & lt) << bit;
+              tot += __popc(bal) << bit;
+            }
+            int o = staged + before;
+            while (un) {
+              const int b = __ffs(un) - 1;
+              un &= un - 1u;
+              uint32_t m = 0;
+#pragma unroll
+              for (int j = 0; j < kGH; ++j) m |= ((bw[j] >> b) & 1u) << j;
+              stage[o & (kStageKeys - 1)] = (w * 32 + b) | (int)(m << 24);
+              ++o;
+            }
+            staged += tot;
+            scan_pos += 32;
+          }
+          __syncwarp();
+          RGS_CHUNK(13, t);
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            const int j = g0 * kChunk + q * 32 + lane;
+            if (j >= u.nk) {
+              pos[q] = -1;
+              memb[q] = 0u;
+            } else if (j < u.blk) {   // block keys: every head
+              pos[q] = u.bs + j;
+              memb[q] = (1u << u.nh) - 1u;
+            } else {
+              const int v = stage[(j - u.blk) & (kStageKeys - 1)];
+              pos[q] = v & 0xffffff;
+              memb[q] = (uint32_t)v >> 24;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            const int j = g0 * kChunk + q * 32 + lane;
+            pos[q] = j < u.nk ? (j < u.blk ? u.bs + j : __ldg(my_idx + (j - u.blk))) : -1;
+          }
         }
         if (g0 == 0 && bt_smem && u.bt_row != bt_cached) {
           __syncwarp();
@@ -252,6 +383,17 @@ reuse_grp_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restr
           ptx::mbar_wait(b_oempty_t + 8 * slot, ((t / kNT) & 1) ^ 1);
 #pragma unroll
           for (int rr = 0; rr < kChunk / 32; ++rr) offs[slot * kChunk + rr * 32 + lane] = off[c * (kChunk / 32) + rr];
+          if constexpr (kUnion) {
+            uint32_t *mk = reinterpret_cast<uint32_t *>(gb + kOffMask) + (t % kRing) * (kGH * (kChunk / 32));
+#pragma unroll
+            for (int rr = 0; rr < kChunk / 32; ++rr) {
+#pragma unroll
+              for (int j = 0; j < kGH; ++j) {
+                const uint32_t bits = __ballot_sync(0xffffffffu, (memb[c * (kChunk / 32) + rr] >> j) & 1u);
+                if (lane == 0) mk[j * (kChunk / 32) + rr] = bits;
+              }
+            }
+          }
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(b_ofull_t + 8 * slot);
           if (t == 0) RGS_CTA(1);
@@ -270,7 +412,7 @@ reuse_grp_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restr
       if (unit >= plan.total_units) break;
       GUnit u;
       gdecode(plan, unit, u);
-      const int nchunks = (u.nk + kChunk - 1) / kChunk;
+      int nchunks = kUnion ? 1 : (u.nk + kChunk - 1) / kChunk;   // union mode: known at the first chunk
       {
         // the sub-group's query rows, head j at tile rows 32j.. (zero rows past the
         // block; rows of absent heads are left as they are: their S^T / O^T columns
@@ -293,6 +435,7 @@ reuse_grp_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restr
       for (int c = 0; c < nchunks; ++c, ++t) {
         const int slot = t % kNT, s = t % NS;
         ptx::mbar_wait(b_ofull_t + 8 * slot, (t / kNT) & 1);
+        if (kUnion && c == 0) nchunks = (reinterpret_cast<const int *>(gb + kOffNk)[i % kRing] + kChunk - 1) / kChunk;
         ptx::mbar_wait(b_kvempty + 8 * s, ((t / NS) & 1) ^ 1);
         const uint32_t dk = sb + s * kStage, dv = dk + kTileK;
 #pragma unroll 4
@@ -306,6 +449,9 @@ reuse_grp_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restr
           cp_async16(dv + so, v_cache + goff, nb);
         }
         cp_async_arrive_noinc(b_kvfull + 8 * s);
+        // (a plain arrive: releases what this lane acquired from the translator -- the
+        // unit's key count and the chunk's membership masks -- to the MMA and softmax warps)
+        if (li == 0 && lane == 0) ptx::mbar_arrive(b_kvfull + 8 * s);
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(b_oempty_t + 8 * slot);
         if (li == 0) RGS_CHUNK(1, t);
@@ -343,7 +489,7 @@ reuse_grp_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restr
       if (unit >= plan.total_units) break;
       GUnit u;
       gdecode(plan, unit, u);
-      const int nchunks = (u.nk + kChunk - 1) / kChunk;
+      int nchunks = kUnion ? 1 : (u.nk + kChunk - 1) / kChunk;
       const int qb = i & 1;
       ptx::mbar_wait(b_qfull + 8 * qb, (i >> 1) & 1);
       for (int c = 0; c < nchunks; ++c, ++t) {
@@ -357,6 +503,8 @@ reuse_grp_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restr
             pv_t = -1;
           }
         }
+        ptx::mbar_wait(b_kvfull + 8 * s, (t / NS) & 1);
+        if (kUnion && c == 0) nchunks = (reinterpret_cast<const int *>(gb + kOffNk)[i % kRing] + kChunk - 1) / kChunk;
         ptx::fence_proxy_async_smem();   // cp.async (generic proxy) data -> tensor core (async proxy)
         ptx::tc_fence_after();
         const uint64_t a0 = dq0 + (uint64_t)((qb * kQTile) >> 4);
@@ -395,7 +543,7 @@ reuse_grp_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restr
       if (unit >= plan.total_units) break;
       GUnit u;
       gdecode(plan, unit, u);
-      const int nchunks = (u.nk + kChunk - 1) / kChunk;
+      int nchunks = kUnion ? 1 : (u.nk + kChunk - 1) / kChunk;
       const int ob = i & 1;
       const bool active = sw < u.nh;
       const uint32_t tO = tmem + lane_base + tm_o(ob);
@@ -406,6 +554,14 @@ reuse_grp_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restr
         ptx::mbar_wait(b_sfull + 8 * b, (t >> 1) & 1);
         ptx::tc_fence_after();
         if (sw == 0) RGS_CHUNK(3, t);
+        if constexpr (kUnion) {
+          // (complete already -- S(t) was issued after it; acquires the translator's data)
+          ptx::mbar_wait(b_kvfull + 8 * (t % NS), (t / NS) & 1);
+          if (c == 0) {
+            u.nk = reinterpret_cast<const int *>(gb + kOffNk)[i % kRing];
+            nchunks = (u.nk + kChunk - 1) / kChunk;
+          }
+        }
         if (active) {
           uint32_t sr[kChunk];
           DLLM_TMEM_LD32(tS + 0, (sr + 0));
@@ -413,11 +569,26 @@ reuse_grp_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restr
           DLLM_TMEM_LD32(tS + 64, (sr + 64));
           ptx::tmem_wait_ld();
           float *x = reinterpret_cast<float *>(sr);
-          const int key_end = u.nk - c * kChunk;   // keys >= key_end of this chunk are padding
-          if (key_end < kChunk) {
+          if constexpr (kUnion) {
+            // keys outside this head's own set (and padding): masked
+            const uint32_t *mk = reinterpret_cast<const uint32_t *>(gb + kOffMask) +
+                                 (t % kRing) * (kGH * (kChunk / 32)) + sw * (kChunk / 32);
 #pragma unroll
-            for (int n = 0; n < kChunk; ++n)
-              if (n >= key_end) x[n] = -INFINITY;
+            for (int rr = 0; rr < kChunk / 32; ++rr) {
+              const uint32_t bits = mk[rr];
+              if (bits != 0xffffffffu) {
+#pragma unroll
+                for (int e = 0; e < 32; ++e)
+                  if (!((bits >> e) & 1u)) x[rr * 32 + e] = -INFINITY;
+              }
+            }
+          } else {
+            const int key_end = u.nk - c * kChunk;   // keys >= key_end of this chunk are padding
+            if (key_end < kChunk) {
+#pragma unroll
+              for (int n = 0; n < kChunk; ++n)
+                if (n >= key_end) x[n] = -INFINITY;
+            }
           }
           float mx;
           {
@@ -579,21 +750,26 @@ int reuse_grp_units(int H, int H_kv, int blk) {
 
 bool reuse_grp_supported(int D) { return D == rgs::kD; }
 
+// union mode keeps per-head position bitmaps of the whole sequence in shared memory
+int reuse_union_max_len() { return rgs::kMaxUnionLen; }
+
 cudaError_t launch_reuse_grp(const Plan &plan, const void *q_blk, const void *k_cache, const void *v_cache,
-                             const int32_t *idx, void *out, cudaStream_t st) {
+                             const int32_t *idx, void *out, bool union_sets, cudaStream_t st) {
   using namespace rgs;
   if (plan.D != kD) return cudaErrorInvalidValue;
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
   std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(reuse_grp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBytes);
+    attr = cudaFuncSetAttribute(reuse_grp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBytes);
+    if (attr == cudaSuccess)
+      attr = cudaFuncSetAttribute(reuse_grp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBytes);
   });
   if (attr != cudaSuccess) return attr;
   const int grid = plan.total_units < num_sms() ? plan.total_units : num_sms();
   if (grid <= 0) return cudaSuccess;
-  return launch_pdl(reuse_grp_kernel, dim3(grid), dim3(kThreads), (size_t)kBytes, st, plan,
-                    (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k_cache, (const __nv_bfloat16 *)v_cache, idx,
-                    (__nv_bfloat16 *)out);
+  return launch_pdl(union_sets ? reuse_grp_kernel<true> : reuse_grp_kernel<false>, dim3(grid), dim3(kThreads),
+                    (size_t)kBytes, st, plan, (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k_cache,
+                    (const __nv_bfloat16 *)v_cache, idx, (__nv_bfloat16 *)out);
 }
 
 }  // namespace dllm

@@ -30,6 +30,14 @@ def reuse_unique_bytes(wl, k, idx_flat):
     return total + extra, logical + extra
 
 
+def _with_env(k, v, f):
+    os.environ[k] = v
+    try:
+        f()
+    finally:
+        del os.environ[k]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("cfg", nargs="?", default="C1")
@@ -50,6 +58,8 @@ def main():
         "refresh": lambda: lib.refresh_attn(p, q, kc, vc, buf.out, buf.scores),
         "select": lambda: lib.select_heads(p, buf.scores, buf.idx),
         "reuse": lambda: lib.reuse_sparse_attn(p, qb, kc, vc, buf.idx, buf.out_blk),
+        "reuse_union": lambda: _with_env("DLLM_REUSE_IMPL", "union",
+                                         lambda: lib.reuse_sparse_attn(p, qb, kc, vc, buf.idx, buf.out_blk)),
         "select_groups": lambda: lib.select_groups(p, buf.scores, gidx),
         "reuse_group_sets": lambda: lib.reuse_group_sets(p, qb, kc, vc, gidx, buf.out_blk),
         "reuse_per_head_on_group_sets": lambda: lib.reuse_sparse_attn(p, qb, kc, vc, gidx, buf.out_blk),
@@ -89,6 +99,9 @@ def main():
     t = res["reuse"][0]
     print(f"{args.cfg} reuse  : {t*1e6:.1f} us  {ub/t/1e9:.1f} GB/s unique ({lb/t/1e9:.1f} logical), "
           f"unique {ub/1e6:.1f} MB")
+    t = res["reuse_union"][0]
+    print(f"{args.cfg} reuse (union of up to 4 heads' sets, DLLM_REUSE_IMPL=union): {t*1e6:.1f} us  "
+          f"{ub/t/1e9:.1f} GB/s unique")
     gub, glb = reuse_unique_bytes(wl, k, gidx.cpu().numpy()[:total_idx])
     t = res["select_groups"][0]
     print(f"{args.cfg} select_groups: {t*1e6:.1f} us")

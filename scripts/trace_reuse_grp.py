@@ -8,7 +8,7 @@ os.environ["DLLM_LIB"] = os.environ.get("DLLM_LIB") or os.path.join(ROOT, "paper
 import torch
 from paper_2512_17077_b200 import lib, synth
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
-n = int(sys.argv[2]) if len(sys.argv) > 2 else None
+n = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] != "all" else None
 wl = synth.config(cfg, num_requests=n)
 b = synth.make_batch(wl)
 p = lib.Problem(wl.seq_len, wl.blk_start, wl.blk_end, num_heads=wl.num_heads, num_kv_heads=wl.num_kv_heads,
@@ -17,13 +17,16 @@ p = lib.Problem(wl.seq_len, wl.blk_start, wl.blk_end, num_heads=wl.num_heads, nu
 q, qb, kc, vc = b.q.cuda(), b.q_blk.cuda(), b.k_cache.cuda(), b.v_cache.cuda()
 buf = lib.alloc_buffers(p)
 lib.refresh_attn(p, q, kc, vc, buf.out, buf.scores)
-lib.select_groups(p, buf.scores, buf.idx)
+union = len(sys.argv) > 3 and sys.argv[3] == "union"   # per-head sets through the union kernel
+(lib.select_heads if union else lib.select_groups)(p, buf.scores, buf.idx)
+run = (lambda: lib.reuse_sparse_attn(p, qb, kc, vc, buf.idx, buf.out_blk)) if union else \
+    (lambda: lib.reuse_group_sets(p, qb, kc, vc, buf.idx, buf.out_blk))
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(3):
     flush.zero_()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    lib.reuse_group_sets(p, qb, kc, vc, buf.idx, buf.out_blk)
+    run()
     e.record()
     torch.cuda.synchronize()
 print("event time us", s.elapsed_time(e) * 1e3)
@@ -51,6 +54,9 @@ print("CTA 0 chunks (us from CTA start): published, loader issued, S issued, sof
       "P arrived, PV issued")
 for t in range(min(24, int((ch[2] > 0).sum()))):
     print(f"  ch{t:3d} " + " ".join(f"{(ch[k, t] - c0) / 1e3:7.2f}" for k in (0, 1, 2, 3, 6, 4, 5)))
+print("translator: union built (per unit), lookups done (per batch, first chunk index)")
+print("  units " + " ".join(f"{(ch[12, u] - c0) / 1e3:7.2f}" for u in range(6) if ch[12, u] > 0))
+print("  batches " + " ".join(f"{t}:{(ch[13, t] - c0) / 1e3:.2f}" for t in range(64) if ch[13, t] > 0))
 print("unit: softmax row sums published, epilogue got O + sums, epilogue stored")
 for u in range(6):
     if ch[9, u] > 0:

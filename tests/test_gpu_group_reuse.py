@@ -68,13 +68,14 @@ def test_reuse_group_sets_parity(L, name):
         assert_close(got[c0:c1], ref, f"{name} group reuse req {b}")
 
 
-def test_reuse_group_sets_matches_per_head_kernel(L):
+def test_reuse_group_sets_matches_per_head_kernel(L, monkeypatch):
     """Same sets through both Reuse kernels: equal within the fp32 rounding of two
     accumulation orders (both are checked against the oracle above)."""
     batch = synth.make_batch(synth.config("C2", num_requests=4))
     k = oracle_keep_counts(batch.wl)
     idx = synth.indices(batch.wl, k, mode="shared")
     a = _run(L, batch, L.reuse_group_sets, idx)
+    monkeypatch.setenv("DLLM_REUSE_IMPL", "tc")
     b = _run(L, batch, L.reuse_sparse_attn, idx)
     assert np.isfinite(a).all()
     d = np.abs(a - b)
@@ -136,3 +137,65 @@ def test_reuse_group_sets_empty_batch(L):
     e = torch.empty(0, dtype=torch.bfloat16, device="cuda")
     L.reuse_group_sets(p, e, e, e, torch.zeros(1, dtype=torch.int32, device="cuda"), e)
     torch.cuda.synchronize()
+
+
+# ------------------------------------------------------------------ union mode (per-head sets, GQA)
+# DLLM_REUSE_IMPL=union: dllm_reuse_sparse_attn runs GQA batches (G >= 2, D = 128,
+# L <= 8192) on the same kernel over the UNION of the sub-group's per-head sets,
+# each head masked to its own keys; longer sequences fall back to the per-head kernel.
+UNION_CASES = {
+    "C2": synth.config("C2", num_requests=3),
+    "g5_ragged": CASES["g5_ragged"],
+    "g8_blk128": CASES["g8_blk128"],
+    "g3_mixed": CASES["g3_mixed"],
+    "g2_p16": CASES["g2_p16"],
+    "g4_blk1_r1": CASES["g4_blk1_r1"],
+    "g7_sparse": custom("u_sparse", [3000, 517], [2900, 480], [2932, 512], H=7, Hk=1, r=0.01),
+    "g4_k0": custom("u_k0", [32, 64], [0, 0], [32, 64], H=4, Hk=1),   # no context keys at all
+    "g7_long": custom("u_long", [8192, 300], [8100, 100], [8132, 132], H=7, Hk=1, r=0.05),
+    "g7_over_union_len": custom("u_over", [9000], [8900], [8932], H=7, Hk=1, r=0.05),   # per-head fallback
+}
+
+
+@pytest.mark.parametrize("name", sorted(UNION_CASES))
+@pytest.mark.parametrize("mode", ["random", "shared"])
+def test_reuse_union_parity(L, name, mode, monkeypatch):
+    monkeypatch.setenv("DLLM_REUSE_IMPL", "union")
+    batch = synth.make_batch(UNION_CASES[name])
+    wl = batch.wl
+    k = oracle_keep_counts(wl)
+    idx = synth.indices(wl, k, mode=mode)
+    got = _run(L, batch, L.reuse_sparse_attn, idx)
+    for b in range(wl.num_requests):
+        ref = O.attention_with_cache(f64(batch.q_blk_req(b)), f64(batch.k_logical(b)), f64(batch.v_logical(b)),
+                                     wl.blk_start[b], wl.blk_end[b], idx[b])
+        c0, c1 = batch.cu_blk[b], batch.cu_blk[b + 1]
+        assert_close(got[c0:c1], ref, f"{name}/{mode} union reuse req {b}")
+
+
+def test_reuse_union_matches_per_head_kernel(L, monkeypatch):
+    batch = synth.make_batch(synth.config("C2", num_requests=4))
+    k = oracle_keep_counts(batch.wl)
+    idx = synth.indices(batch.wl, k)
+    monkeypatch.setenv("DLLM_REUSE_IMPL", "union")
+    a = _run(L, batch, L.reuse_sparse_attn, idx)
+    monkeypatch.setenv("DLLM_REUSE_IMPL", "tc")
+    b = _run(L, batch, L.reuse_sparse_attn, idx)
+    d = np.abs(a - b)
+    assert np.isfinite(a).all() and d.max() <= 8e-3 and d.mean() <= 2e-4, (d.max(), d.mean())
+
+
+def test_reuse_union_full_c2_sampled(L, monkeypatch):
+    """The full C2 batch with per-head sets through the union kernel."""
+    monkeypatch.setenv("DLLM_REUSE_IMPL", "union")
+    batch = synth.make_batch(synth.config("C2"))
+    wl = batch.wl
+    k = oracle_keep_counts(wl)
+    idx = synth.indices(wl, k)
+    got = _run(L, batch, L.reuse_sparse_attn, idx)
+    assert np.isfinite(got).all()
+    for b in (0, 17, wl.num_requests - 1):
+        ref = O.attention_with_cache(f64(batch.q_blk_req(b)), f64(batch.k_logical(b)), f64(batch.v_logical(b)),
+                                     wl.blk_start[b], wl.blk_end[b], idx[b])
+        c0, c1 = batch.cu_blk[b], batch.cu_blk[b + 1]
+        assert_close(got[c0:c1], ref, f"C2 full union reuse req {b}")
