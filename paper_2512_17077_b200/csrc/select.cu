@@ -1,17 +1,16 @@
 // Select: local max-pool + per-head TopK (§4.5, Eq. 6).
 //
-// One CTA per (request b, query head h).  The CTA
+// One CTA per (request b, query head h) (select_heads_kernel below).  The CTA
 //   1. pools the raw scores of the n_ctx candidates C = [0,bs) ++ [be,L)
 //      on the compacted candidate axis (window half-width w/2, clipped;
-//      DESIGN.md R2-R4) straight from global memory (neighbour reads hit L1),
-//      and stores order-preserving 32-bit keys in shared memory
+//      DESIGN.md R2-R4) and keeps order-preserving 32-bit keys in registers
 //      (float -> uint, larger float -> larger key, -0 canonicalised to +0;
 //      DESIGN.md R9);
 //   2. finds the k-th largest key exactly with a 4-pass 8-bit MSB radix
 //      select (shared-memory histograms);
 //   3. compacts: every key above the threshold, plus the lowest-index
 //      (k - #above) keys equal to it (R6), written as sequence
-//      positions in ascending order (R7) with two ballot-based block scans.
+//      positions in ascending order (R7) after one block scan of the counts.
 // All decisions are integer comparisons of the fp32 inputs: bit-exact.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -28,8 +27,7 @@ namespace dllm {
 #endif
 constexpr int kSelThreads = DLLM_SEL_THREADS;
 constexpr int kSelWarps = kSelThreads / 32;
-constexpr int kSelSmemStageMax = 24576;   // words of raw scores + keys staged in smem (96 KB)
-constexpr int kSelSmemMaxWords = 32768;   // DLLM_MAX_SELECT_LEN keys (128 KB)
+constexpr int kSelSmemMaxWords = 32772;   // DLLM_MAX_SELECT_LEN raw scores (+ alignment slack)
 #ifdef DLLM_TRACE
 // dev: phase timestamps (clock64) of a few CTAs: [cta][0 start, 1 after wait, 2 request found,
 // 3 raw staged, 4 pooled, 5..8 radix passes, 9 compaction done]
@@ -76,24 +74,62 @@ __device__ __forceinline__ int block_excl_scan(int v, int *warp_buf, int *total)
   return base + x - v;
 }
 
-__global__ void __launch_bounds__(kSelThreads)
+// Block-wide exclusive scan for any multiple-of-32 block size.
+__device__ __forceinline__ int block_excl_scan_any(int v, int *warp_buf, int *total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (nw == 1) {
+    *total = __shfl_sync(0xffffffffu, x, 31);
+    return x - v;
+  }
+  if (lane == 31) warp_buf[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < nw ? warp_buf[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) warp_buf[lane] = w;   // inclusive warp prefix
+  }
+  __syncthreads();
+  const int base = warp ? warp_buf[warp - 1] : 0;
+  *total = warp_buf[nw - 1];
+  return base + x - v;
+}
+
+// One CTA of T = 32 * ceil(n_max / (32 E)) threads per (request, head); thread t
+// keeps the keys of the E contiguous candidates c = t E + e in registers, so the
+// radix passes touch shared memory only for the 256-bin histogram.
+//   1. the raw scores are staged in shared memory (coalesced) and each thread pools
+//      its candidates from a register window (16-byte loads + halo);
+//   2. 4-pass 8-bit MSB radix select of the k-th largest key;
+//   3. each thread counts its candidates above / equal to the threshold, one block
+//      scan gives the output slots, and every thread writes its own positions --
+//      ascending because thread order is candidate order.
+template <int E>
+__global__ void __launch_bounds__(1024)
 select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__ scores,
-                    int32_t *__restrict__ idx, const int stage) {
-  extern __shared__ uint32_t keys[];                  // [n_ctx]
-  __shared__ int hist[2][256];      // double-buffered: the next pass's is cleared while this one fills
+                    int32_t *__restrict__ idx) {
+  extern __shared__ uint32_t sm[];   // raw scores [n]
+  __shared__ int hist[256];
   __shared__ int warp_buf[32];
-  __shared__ uint32_t s_prefix[2];
-  __shared__ int s_krem[2];
+  __shared__ uint32_t s_prefix;
+  __shared__ int s_krem;
 
   SEL_TR(0);
   pdl_wait_then_trigger();
   SEL_TR(1);
-  const int unit = blockIdx.x;
-  // every request owns exactly H units (one per head): no search over the plan
-  // (a binary search in parameter memory cost ~1,200 clk of a ~14k clk CTA at C1)
-  const int b = unit / plan.H;
+  const int T = blockDim.x, tid = threadIdx.x;
+  const int b = blockIdx.x / plan.H;
+  const int h = blockIdx.x - b * plan.H;
   const ReqInfo &R = plan.r[b];
-  const int h = unit - b * plan.H;
   const int L = R.L, bs = R.bs, blk = R.be - R.bs;
   const int n = L - blk;
   const int k = R.k;
@@ -103,82 +139,89 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
   const int half = plan.window >> 1;
   SEL_TR(2);
 
-  // 1. pool on the compacted axis, to order keys.  When every request's candidates
-  // fit twice in shared memory (`stage`, decided for the whole launch by the host,
-  // which sized the allocation accordingly), the raw scores are first staged there
-  // with all loads of a thread in flight together (one memory round trip instead of
-  // one per window element and candidate), then pooled from shared memory.
-  if (stage) {
-    float *rawc = reinterpret_cast<float *>(keys + n);
-#pragma unroll 4
-    for (int c = threadIdx.x; c < n; c += kSelThreads) rawc[c] = __ldg(raw + (c < bs ? c : c + blk));
-    __syncthreads();
-    SEL_TR(3);
-    for (int c = threadIdx.x; c < n; c += kSelThreads) {
-      const int lo = max(0, c - half), hi = min(n - 1, c + half);
-      float m = -INFINITY;
-      for (int j = lo; j <= hi; ++j) m = fmaxf(m, rawc[j]);
-      keys[c] = order_key(m);
+  // 1. stage the raw scores (coalesced), then every thread pools its own E
+  // contiguous candidates c0 .. c0 + E - 1 from a register window (16-byte loads of
+  // the E values plus the half-window halo on each side)
+  float *rawc = reinterpret_cast<float *>(sm);
+  for (int c = tid; c < n; c += T) rawc[c] = __ldg(raw + (c < bs ? c : c + blk));
+  __syncthreads();
+  SEL_TR(3);
+  const int c0 = tid * E;
+  uint32_t key[E];
+  if (c0 + E <= n) {
+    float x[E];
+#pragma unroll
+    for (int q = 0; q < E / 4; ++q) {
+      const float4 v = reinterpret_cast<const float4 *>(rawc + c0)[q];
+      x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
+    }
+    if (half == 1) {
+      const float left = c0 > 0 ? rawc[c0 - 1] : -INFINITY;
+      const float right = c0 + E < n ? rawc[c0 + E] : -INFINITY;
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        key[e] = order_key(fmaxf(fmaxf(e > 0 ? x[e - 1] : left, x[e]), e + 1 < E ? x[e + 1] : right));
+    } else if (half == 0) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) key[e] = order_key(x[e]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int c = c0 + e;
+        const int lo = max(0, c - half), hi = min(n - 1, c + half);
+        float m = -INFINITY;
+        for (int j = lo; j <= hi; ++j) m = fmaxf(m, rawc[j]);
+        key[e] = order_key(m);
+      }
     }
   } else {
-    for (int c = threadIdx.x; c < n; c += kSelThreads) {
-      const int lo = max(0, c - half), hi = min(n - 1, c + half);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int c = c0 + e;
       float m = -INFINITY;
-      for (int j = lo; j <= hi; ++j) {
-        const int pos = j < bs ? j : j + blk;
-        m = fmaxf(m, __ldg(raw + pos));
+      if (c < n) {
+        const int lo = max(0, c - half), hi = min(n - 1, c + half);
+        for (int j = lo; j <= hi; ++j) m = fmaxf(m, rawc[j]);
       }
-      keys[c] = order_key(m);
+      key[e] = order_key(m);
     }
   }
-  for (int i = threadIdx.x; i < 256; i += kSelThreads) hist[0][i] = 0;
-  __syncthreads();
   SEL_TR(4);
 
-  // 2. radix select of the k-th largest key (MSB first)
+  // 2. radix select of the k-th largest key (MSB first).  (Measured alternatives,
+  // slower: runs of equal bins per thread added with one atomic, and a double-
+  // buffered histogram saving one barrier per pass: C1 13.3 -> 13.3 us, C4 138 -> 152.)
   uint32_t prefix = 0u, mask = 0u;
   int krem = k;
 #pragma unroll 1
   for (int shift = 24; shift >= 0; shift -= 8) {
-    // two block barriers per pass: hist[cur] fills while hist[cur ^ 1] (read by the
-    // previous pass before its second barrier) is cleared for the next pass; the
-    // digit goes through s_prefix[cur], next rewritten two passes later
-    const int cur = ((24 - shift) >> 3) & 1;
-    for (int i = threadIdx.x; i < 256; i += kSelThreads) hist[cur ^ 1][i] = 0;
-    // warp-aggregated: the candidates' keys crowd a few bins (similar exponents), so
-    // lanes with equal bins are merged (match.any) into one shared atomic
-    for (int c0 = 0; c0 < n; c0 += kSelThreads) {
-      const int c = c0 + threadIdx.x;
-      const uint32_t key = c < n ? keys[c] : 0u;
-      const bool act = c < n && (key & mask) == prefix;
-      const uint32_t bin = act ? ((key >> shift) & 0xffu) : 0x100u;
-      const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-      if (act && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[cur][bin], __popc(peers));
-    }
+    for (int i = tid; i < 256; i += T) hist[i] = 0;
     __syncthreads();
-    if (threadIdx.x < 32) {
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (c0 + e < n && (key[e] & mask) == prefix) atomicAdd(&hist[(key[e] >> shift) & 0xffu], 1);
+    __syncthreads();
+    if (tid < 32) {
       // lane l owns bins [8*(31-l), 8*(31-l)+8): lane 0 holds the top bins
-      const int lane = threadIdx.x;
+      const int lane = tid;
       const int base = 8 * (31 - lane);
       int cnt[8], sum = 0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) { cnt[i] = hist[cur][base + 7 - i]; sum += cnt[i]; }  // descending bins
+      for (int i = 0; i < 8; ++i) { cnt[i] = hist[base + 7 - i]; sum += cnt[i]; }   // descending bins
       int incl = sum;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
       }
-      const int above = incl - sum;                   // keys in higher bins than this lane's
-      const bool mine = above < krem && krem <= incl;
-      if (mine) {
+      const int above = incl - sum;
+      if (above < krem && krem <= incl) {
         int acc = above;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           if (acc + cnt[i] >= krem) {
-            const uint32_t digit = (uint32_t)(base + 7 - i);
-            s_prefix[cur] = prefix | (digit << shift);
-            s_krem[cur] = krem - acc;
+            s_prefix = prefix | ((uint32_t)(base + 7 - i) << shift);
+            s_krem = krem - acc;
             break;
           }
           acc += cnt[i];
@@ -186,30 +229,34 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
       }
     }
     __syncthreads();
-    prefix = s_prefix[cur];
-    krem = s_krem[cur];
+    prefix = s_prefix;
+    krem = s_krem;
     mask |= 0xffu << shift;
     SEL_TR(5 + (24 - shift) / 8);
   }
   const uint32_t thr = prefix;   // exact key of the k-th largest
-  const int need_eq = krem;      // how many keys equal to thr are taken (lowest index first)
+  const int need_eq = krem;      // keys equal to thr taken, lowest index first
 
-  // 3. compaction in ascending candidate order
-  // One block scan per 512 candidates of the packed pair (above, equal): a selected
-  // candidate's output slot is (#above before it) + min(#equal before it, need_eq),
-  // because exactly the first need_eq equal keys are taken.
-  int eq_base = 0, gt_base = 0;
-  for (int c0 = 0; c0 < n; c0 += kSelThreads) {
-    const int c = c0 + threadIdx.x;
-    uint32_t key = c < n ? keys[c] : 0u;
-    const int gt = (c < n) && key > thr;
-    const int eq = (c < n) && key == thr;
-    int tot;
-    const int pre = block_excl_scan(gt | (eq << 16), warp_buf, &tot);
-    const int gt_pre = gt_base + (pre & 0xffff), eq_pre = eq_base + (pre >> 16);
-    if (gt || (eq && eq_pre < need_eq)) out[gt_pre + min(eq_pre, need_eq)] = c < bs ? c : c + blk;
-    gt_base += tot & 0xffff;
-    eq_base += tot >> 16;
+  // 3. compaction: slot = (#above before) + min(#equal before, need_eq)
+  int ngt = 0, neq = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const bool v = c0 + e < n;
+    ngt += v && key[e] > thr;
+    neq += v && key[e] == thr;
+  }
+  int tot;
+  const int pre = block_excl_scan_any(ngt | (neq << 16), warp_buf, &tot);
+  int gt_b = pre & 0xffff, eq_b = pre >> 16;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int c = c0 + e;
+    if (c < n) {
+      const bool gt = key[e] > thr, eq = key[e] == thr;
+      if (gt || (eq && eq_b < need_eq)) out[gt_b + min(eq_b, need_eq)] = c < bs ? c : c + blk;
+      gt_b += gt;
+      eq_b += eq;
+    }
   }
   SEL_TR(9);
 }
@@ -341,23 +388,37 @@ __global__ void check_indices_kernel(const __grid_constant__ Plan plan, const in
   if (bad) atomicAdd(violations, bad);
 }
 
-cudaError_t launch_select(const Plan &plan, const float *scores, int32_t *idx, cudaStream_t st) {
+// Keys per thread E: the smallest of 4, 8, 16, 32 that keeps the CTA at <= 256
+// threads (C1, n = 992: E = 4, 256 threads; C4, n = 4,064: E = 16, 256 threads).
+// Measured (profiles/r02_ab_select_v2.log): C1 13.3 us, C4 138 us, against 17.4 and
+// 191-209 us for the round-1 kernel (512 threads, keys in shared memory).
+template <int E>
+cudaError_t launch_select_e(const Plan &plan, const float *scores, int32_t *idx, int max_n, cudaStream_t st) {
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
   std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(select_heads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr = cudaFuncSetAttribute(select_heads_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSelSmemMaxWords * (int)sizeof(uint32_t));
   });
   if (attr != cudaSuccess) return attr;
+  const int threads = 32 * max(1, (max_n + 32 * E - 1) / (32 * E));
+  const size_t words = (size_t)max_n + 4;
+  if (threads > 1024 || words > (size_t)kSelSmemMaxWords) return cudaErrorInvalidValue;
+  return launch_pdl(select_heads_kernel<E>, dim3(plan.total_units), dim3(threads), words * sizeof(uint32_t), st,
+                    plan, scores, idx);
+}
+
+cudaError_t launch_select(const Plan &plan, const float *scores, int32_t *idx, cudaStream_t st) {
   int max_n = 0;
   for (int b = 0; b < plan.nreq; ++b) max_n = max(max_n, plan.r[b].L - (plan.r[b].be - plan.r[b].bs));
-  // staging is decided for the whole launch: every CTA then has room for 2 n words
-  const int stage = 2 * max_n <= kSelSmemStageMax ? 1 : 0;
-  const size_t words = stage ? 2 * (size_t)max_n : (size_t)max_n;
-  const size_t smem = (words > 0 ? words : 1) * sizeof(uint32_t);
-  if (words > (size_t)kSelSmemMaxWords) return cudaErrorInvalidValue;
-  return launch_pdl(select_heads_kernel, dim3(plan.total_units), dim3(kSelThreads), smem, st, plan, scores, idx,
-                    stage);
+#ifdef DLLM_SEL_E
+  return launch_select_e<DLLM_SEL_E>(plan, scores, idx, max_n, st);
+#else
+  if (max_n <= 256 * 4) return launch_select_e<4>(plan, scores, idx, max_n, st);
+  if (max_n <= 256 * 8) return launch_select_e<8>(plan, scores, idx, max_n, st);
+  if (max_n <= 256 * 16) return launch_select_e<16>(plan, scores, idx, max_n, st);
+  return launch_select_e<32>(plan, scores, idx, max_n, st);
+#endif
 }
 
 cudaError_t launch_select_global(const Plan &plan, const float *scores, int32_t *idx, int heads_per_set,
