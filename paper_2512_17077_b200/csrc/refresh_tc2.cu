@@ -93,7 +93,10 @@ static_assert(2 * DLLM_TC2_REG_SOFTMAX + DLLM_TC2_REG_EPI <= 448, "register budg
 // Measured in round 1 and removed: L2 prefetch of the next unit's K/V and Q
 // (slower), next-unit decode mid-unit, one barrier pair per K/V stage, an MMA warp
 // serving the two Q tiles in P-ready order (4-5% slower), a request cursor in
-// decode_unit (0.5-1% slower), other warp-role placements (neutral).
+// decode_unit (0.5-1% slower), other warp-role placements (neutral).  Round 2: softmax
+// warpgroup 1 held until warpgroup 0 finished each step's row max (to put the two
+// exponential phases out of phase on the shared MUFU): C1 280 vs 272, C2 1,658 vs
+// 1,584 us (profiles/r02_ab_tc2_skew.log).
 #ifndef DLLM_TC2_FUSEDSEL
 // 1: pool + TopK fused into the epilogue warpgroup (dllm_refresh_select_attn).  Off by
 // default: measured ~13 us per (b, h) selection at C1 (~25k clk, issue-starved beside
@@ -114,7 +117,8 @@ struct Cfg {
   static constexpr int kOffBar = kOffSc + 2 * 2 * 4 * TBN * 4;
   static constexpr int kOffStage = kOffBar + 1024;       // [4 epilogue warps][32 rows][64 B] staging (SW64)
   static constexpr int kOffL = kOffStage + 4 * 32 * 64;  // [2 parity][2 tiles][128] f32 row sums
-  static constexpr int kOffReq = kOffL + 2 * 2 * 128 * 4;
+  static constexpr int kOffUnits = kOffL + 2 * 2 * 128 * 4;  // [kUnitRing][128 B] decoded units (K/V producer -> roles)
+  static constexpr int kOffReq = kOffUnits + 4 * 128;
   // + nreq * sizeof(ReqInfo) + 1024 alignment slack, sized per launch
   static int bytes(int nreq) { return kOffReq + nreq * (int)sizeof(ReqInfo) + 1024; }
 };
@@ -157,14 +161,10 @@ struct Unit {
   int64_t idx_off;
 };
 
-// a / b and a % b for 0 <= a < 2^24, 1 <= b < 2^24: fp32 quotient (off by at most
-// one) and one integer correction -- about a tenth of the latency of the integer
-// division sequence, which sat on the unit-boundary critical path of every role
-
-// `cur` is the caller's cursor into the request table: every role walks its units
-// in increasing order, so the owning request is found by advancing the cursor
-// (usually 0 or 1 step) instead of a binary search
-__device__ __forceinline__ void decode_unit(const Plan &pl, const ReqInfo *rs, int unit, Unit &u, int &cur) {
+// Work unit -> request (binary search over the request table in shared memory),
+// head, Q-tile pair and importance-epilogue flags.  Called once per unit by the
+// K/V producer only; the other roles receive the decoded Unit through shared memory.
+__device__ __forceinline__ void decode_unit(const Plan &pl, const ReqInfo *rs, int unit, Unit &u) {
   int lo = 0, hi = pl.nreq - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -363,7 +363,6 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
   uint8_t *gb = smem_raw + (sb - raw_u32);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto bar = [&](int i) { return sb + C::kOffBar + 8u * (uint32_t)i; };
-  int dcur = 0;   // request-table cursor of decode_unit (per thread)
 
 #ifdef DLLM_TRACE
   if (threadIdx.x == 0 && blockIdx.x < 1024) { g_cta2[blockIdx.x][0] = gtimer(); g_cta2[blockIdx.x][2] = 0; }
@@ -416,17 +415,22 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
   // without one the units go round-robin
   const bool dyn = kDynSched && plan.sched != nullptr;
   volatile int *ring = reinterpret_cast<volatile int *>(gb + C::kOffBar + kRingOff);
-  // i-th unit of this CTA as seen by a reader role (static: cta + i * ncta).  A whole
+  Unit *uring = reinterpret_cast<Unit *>(gb + C::kOffUnits);
+  // i-th unit of this CTA as seen by a reader role: the K/V producer claims it
+  // (statically: cta + i * ncta; dynamically: from the device counter), decodes it
+  // once and publishes id + decoded Unit through a kRing-slot shared-memory ring, so
+  // the unit-boundary critical paths of the other roles carry no decode (measured
+  // ~1,150 clk per decode_unit in every role, scripts/trace_refresh2.py).  A whole
   // warp reads the slot and lane 0 releases it after __syncwarp; a single-thread
   // role (the Q producer) reads and releases it alone.
-  auto unit_at = [&](int i, bool whole_warp) -> int {
-    if (!dyn) return cta + i * ncta;
+  auto unit_at = [&](int i, bool whole_warp, Unit &u) -> int {
     const int slot = i % kRing;
     ptx::mbar_wait(bar(B_RFULL + slot), (i / kRing) & 1);
-    const int u = ring[slot];
+    const int un = ring[slot];
+    if (un < plan.total_units) u = uring[slot];
     if (whole_warp) __syncwarp();
     if (!whole_warp || lane == 0) ptx::mbar_arrive(bar(B_REMPTY + slot));
-    return u;
+    return un;
   };
 
   if (warp == kProducerWarp) {
@@ -436,30 +440,37 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
     const int boxrows = plan.page_size < TBN ? plan.page_size : TBN;
     const int nsub = TBN / boxrows;
     const uint32_t boxbytes = (uint32_t)boxrows * 128u;
-    // the next unit is decoded mid-unit (off the unit-boundary critical path)
-    Unit un;
-    if (cta < plan.total_units) decode_unit(plan, rs, cta, un, dcur);
     auto claim = [&]() {
       const int c = ncta + atomicAdd(plan.sched, 1);
       return c < plan.total_units ? c : plan.total_units;
     };
     for (int i = 0;; ++i, ++ucnt) {
-      int unit = cta + i * ncta;
-      if (dyn) {
-        // this role needs the next unit first: claim it and publish it to the others
-        if (lane == 0) {
-          unit = i == 0 ? cta : claim();
-          unit = unit < plan.total_units ? unit : plan.total_units;
-          const int slot = i % kRing;
-          ptx::mbar_wait(bar(B_REMPTY + slot), ((i / kRing) & 1) ^ 1);
-          ring[slot] = unit;
-          ptx::mbar_arrive(bar(B_RFULL + slot));
+      // this role needs the next unit first: claim it, decode it, publish it
+      int unit = 0;
+      if (lane == 0) {
+        unit = i == 0 ? cta : (dyn ? claim() : cta + i * ncta);
+        unit = unit < plan.total_units ? unit : plan.total_units;
+      }
+      unit = __shfl_sync(0xffffffffu, unit, 0);
+      Unit u;
+      if (unit < plan.total_units) decode_unit(plan, rs, unit, u);
+      if (lane == 0) {
+        if (i > 0 && unit < plan.total_units) {
+          // the unit's Q tiles go to L2 now, ~NST steps before the Q producer can load
+          // them (after the current unit's last Q.K^T): the MMA warp's cross-unit
+          // lookahead needs them ~1 step after that, and an HBM-cold 64 KB Q load took
+          // ~2,900 clk there (trace)
+          for (int t = 0; t < (u.tile1 ? 2 : 1); ++t)
+            for (int c = 0; c < C::kChunks; ++c)
+              ptx::tma_prefetch_3d(&tm_q, c * 64, u.h, u.q_off + (t ? u.origin1 : u.origin0));
         }
-        unit = __shfl_sync(0xffffffffu, unit, 0);
+        const int slot = i % kRing;
+        ptx::mbar_wait(bar(B_REMPTY + slot), ((i / kRing) & 1) ^ 1);
+        ring[slot] = unit;
+        if (unit < plan.total_units) uring[slot] = u;
+        ptx::mbar_arrive(bar(B_RFULL + slot));
       }
       if (unit >= plan.total_units) break;
-      decode_unit(plan, rs, unit, un, dcur);
-      const Unit u = un;
       const int32_t *bt = plan.block_table + (int64_t)u.bt_row * plan.pages_per_req;
       for (int j = 0; j < u.n; ++j, ++it) {
         const int s = it % NST;
@@ -519,13 +530,10 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
     // not queued behind the wait for the Q buffers to drain)
     if (lane == 0) {
       int ucnt = 0;
-      Unit un;
-      if (cta < plan.total_units) decode_unit(plan, rs, cta, un, dcur);
       for (int i = 0;; ++i, ++ucnt) {
-        const int unit = unit_at(i, false);
+        Unit u;
+        const int unit = unit_at(i, false, u);
         if (unit >= plan.total_units) break;
-        decode_unit(plan, rs, unit, un, dcur);
-        const Unit u = un;
         TRACE2(20, ucnt);
         ptx::mbar_wait(bar(B_QEMPTY), (ucnt & 1) ^ 1);
         TRACE2(21, ucnt);
@@ -553,96 +561,133 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
       int gs[2] = {0, 0};        // S tiles issued per Q tile (buffer = gs & 1)
       int gp[2] = {0, 0};        // P.V issued per Q tile
       int ou[2] = {0, 0};        // units per Q tile (O accumulator reuse)
-      Unit un;
-      if (cta < plan.total_units) decode_unit(plan, rs, cta, un, dcur);
-      for (int i = 0;; ++i, ++ucnt) {
-        const int unit = unit_at(i, true);
-        if (unit >= plan.total_units) break;
-        if (lane == 0) TRACE2(23, 2 * ucnt);
-        decode_unit(plan, rs, unit, un, dcur);
-        const Unit u = un;
-        if (lane == 0) TRACE2(23, 2 * ucnt + 1);
-        const int nt = u.tile1 ? 2 : 1;
-        auto qk = [&](int i, int stage) {
-          const int b = gs[i] & 1;
-          const uint64_t a0 = dq + (uint64_t)((i * C::kQBytes) >> 4);
-          const uint64_t b0 = dk + (uint64_t)((stage * C::kKVBytes) >> 4);
+      auto qk = [&](int i, int stage) {
+        const int b = gs[i] & 1;
+        const uint64_t a0 = dq + (uint64_t)((i * C::kQBytes) >> 4);
+        const uint64_t b0 = dk + (uint64_t)((stage * C::kKVBytes) >> 4);
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint32_t ko = (uint32_t)(((k >> 2) * TBM * 128 + (k & 3) * 32) >> 4);
-            const uint32_t kb = (uint32_t)(((k >> 2) * TBN * 128 + (k & 3) * 32) >> 4);
-            ptx::mma_ss_elect(tmem + tmem_s(i, b), a0 + ko, b0 + kb, idesc_qk, k > 0);
-          }
-          ptx::mma_commit_elect(bar(B_SFULL + 2 * i + b));
-          ++gs[i];
-        };
-        auto pv = [&](int i, int stage, bool acc, bool last) {
-          const int b = gp[i] & 1;
-          const uint64_t v0 = dv + (uint64_t)((stage * C::kKVBytes) >> 4);
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t ko = (uint32_t)(((k >> 2) * TBM * 128 + (k & 3) * 32) >> 4);
+          const uint32_t kb = (uint32_t)(((k >> 2) * TBN * 128 + (k & 3) * 32) >> 4);
+          ptx::mma_ss_elect(tmem + tmem_s(i, b), a0 + ko, b0 + kb, idesc_qk, k > 0);
+        }
+        ptx::mma_commit_elect(bar(B_SFULL + 2 * i + b));
+        ++gs[i];
+      };
+      auto pv = [&](int i, int stage, bool acc, bool last) {
+        const int b = gp[i] & 1;
+        const uint64_t v0 = dv + (uint64_t)((stage * C::kKVBytes) >> 4);
 #pragma unroll
-          for (int k = 0; k < TBN / 16; ++k)
-            ptx::mma_ts_elect(tmem + tmem_o(i), tmem + tmem_s(i, b) + (uint32_t)(k * 8), v0 + (uint64_t)((k * 16 * 128) >> 4),
-                              idesc_pv, (acc || k > 0) ? 1u : 0u);
-          ptx::mma_commit_elect(bar(B_ODONE + 2 * i + b));
-          if (last) ptx::mma_commit_elect(bar(B_OFULL + i));
-          ++gp[i];
-        };
-        if (lane == 0) TRACE2(16, ucnt);
-        ptx::mbar_wait(bar(B_QFULL), ucnt & 1);
-        if (lane == 0) TRACE2(17, ucnt);
+        for (int k = 0; k < TBN / 16; ++k)
+          ptx::mma_ts_elect(tmem + tmem_o(i), tmem + tmem_s(i, b) + (uint32_t)(k * 8), v0 + (uint64_t)((k * 16 * 128) >> 4),
+                            idesc_pv, (acc || k > 0) ? 1u : 0u);
+        ptx::mma_commit_elect(bar(B_ODONE + 2 * i + b));
+        if (last) ptx::mma_commit_elect(bar(B_OFULL + i));
+        ++gp[i];
+      };
+      // One continuous stream of 64-key steps over the CTA's units: at P.V step g the
+      // MMA warp issues S(g + 2), also when step g + 2 belongs to the NEXT unit (its Q
+      // tiles permitting: the Q buffer is refilled after the current unit's last Q.K^T,
+      // checked without blocking).  Without this cross-unit lookahead every unit
+      // boundary cost ~2,600-3,000 clk of softmax idle time (S'(0) issued only after the
+      // last P.V of the previous unit): 8-11% of a C1 unit (scripts/trace_refresh2.py).
+      Unit cu, nu;
+      if (lane == 0) TRACE2(23, 0);
+      int cur_id = unit_at(0, true, cu);
+      int q_issued = 0;          // Q.K^T steps of cu already issued by the previous unit's lookahead
+      bool q_ready = false;      // QFULL of cu acquired
+      while (cur_id < plan.total_units) {
+        const int nt = cu.tile1 ? 2 : 1;
+        if (!q_ready) {
+          if (lane == 0) TRACE2(16, ucnt);
+          ptx::mbar_wait(bar(B_QFULL), ucnt & 1);
+          if (lane == 0) TRACE2(17, ucnt);
+        }
         ptx::tc_fence_after();
-        // prologue: S(0) and S(1) of every tile
-        const int npro = u.n < 2 ? u.n : 2;
-        for (int jj = 0; jj < npro; ++jj) {
+        // prologue: S(0) and S(1) of every tile, unless the lookahead issued them
+        const int npro = cu.n < 2 ? cu.n : 2;
+        for (int jj = q_issued; jj < npro; ++jj) {
           const int st = (it + jj) % NST;
           ptx::mbar_wait(bar(B_KFULL + st), ((it + jj) / NST) & 1);
           if (lane == 0) TRACE2(18 + jj, ucnt);
           ptx::tc_fence_after();
           for (int i = 0; i < nt; ++i) qk(i, st);
           ptx::mma_commit_elect(bar(B_KEMPTY + st));
+          if (jj == cu.n - 1) ptx::mma_commit_elect(bar(B_QEMPTY));
         }
-        if (u.n <= 2) ptx::mma_commit_elect(bar(B_QEMPTY));
-        for (int j = 0; j < u.n; ++j) {
+        int nxt_id = -1;         // next unit, read from the ring when the lookahead reaches it
+        int nq = 0;              // Q.K^T steps of nu issued below
+        bool nq_ready = false;
+        for (int j = 0; j < cu.n; ++j) {
           const int sv = (it + j) % NST;
           if (lane == 0) TRACE2(10, it + j);
           ptx::mbar_wait(bar(B_VFULL + sv), ((it + j) / NST) & 1);
           if (lane == 0) TRACE2(11, it + j);
-          if (j == u.n - 1 && (u.L % TBN) != 0) {
+          if (j == cu.n - 1 && (cu.L % TBN) != 0) {
             ptx::mbar_wait(bar(B_VZ), vzc & 1);
             ++vzc;
           }
-          const bool ahead = j + 2 < u.n;
-          const int sk = (it + j + 2) % NST;
-          for (int i = 0; i < nt; ++i) {
-            const int b = gp[i] & 1;
-            if (lane == 0) TRACE2(6 + 2 * i, gp[i]);
-            ptx::mbar_wait(bar(B_PFULL + 2 * i + b), (gp[i] >> 1) & 1);
-            if (lane == 0) TRACE2(7 + 2 * i, gp[i]);
-            if (j == 0) {
-              // the epilogue warpgroup must have read the previous unit's O_i
-              ptx::mbar_wait(bar(B_OFREE + i), (ou[i] & 1) ^ 1);
-              ++ou[i];
+          // the lookahead Q.K^T of this step: global step it + j + 2
+          int tg_nt = 0, tg_last = 0;
+          bool tg_next = false;
+          if (j + 2 < cu.n) {
+            tg_nt = nt;
+            tg_last = j + 2 == cu.n - 1;
+          } else {
+            if (nxt_id < 0) {
+              if (lane == 0) TRACE2(23, 2 * ucnt + 1);
+              nxt_id = unit_at(ucnt + 1, true, nu);
             }
-            ptx::tc_fence_after();
-            pv(i, sv, j > 0, j == u.n - 1);
-            if (ahead) {
+            if (nxt_id < plan.total_units && nq < nu.n && nq <= j + 2 - cu.n) {
+              if (!nq_ready) nq_ready = ptx::mbar_test_wait(bar(B_QFULL), (ucnt + 1) & 1);
+              if (nq_ready) {
+                tg_next = true;
+                tg_nt = nu.tile1 ? 2 : 1;
+                tg_last = nq == nu.n - 1;
+              }
+            }
+          }
+          const int gk = it + (tg_next ? cu.n + nq : j + 2);
+          const int sk = gk % NST;
+          for (int i = 0; i < 2; ++i) {
+            if (i < nt) {
+              const int b = gp[i] & 1;
+              if (lane == 0) TRACE2(6 + 2 * i, gp[i]);
+              ptx::mbar_wait(bar(B_PFULL + 2 * i + b), (gp[i] >> 1) & 1);
+              if (lane == 0) TRACE2(7 + 2 * i, gp[i]);
+              if (j == 0) {
+                // the epilogue warpgroup must have read the previous unit's O_i
+                ptx::mbar_wait(bar(B_OFREE + i), (ou[i] & 1) ^ 1);
+                ++ou[i];
+              }
+              ptx::tc_fence_after();
+              pv(i, sv, j > 0, j == cu.n - 1);
+            }
+            if (i < tg_nt) {
               if (i == 0) {
                 if (lane == 0) TRACE2(12, it + j);
-                ptx::mbar_wait(bar(B_KFULL + sk), ((it + j + 2) / NST) & 1);
+                ptx::mbar_wait(bar(B_KFULL + sk), (gk / NST) & 1);
                 if (lane == 0) TRACE2(13, it + j);
                 ptx::tc_fence_after();
               }
               qk(i, sk);
             }
           }
-          if (ahead) {
+          if (tg_nt > 0) {
             ptx::mma_commit_elect(bar(B_KEMPTY + sk));
-            if (j + 2 == u.n - 1) ptx::mma_commit_elect(bar(B_QEMPTY));
+            if (tg_last) ptx::mma_commit_elect(bar(B_QEMPTY));
+            if (tg_next) ++nq;
           }
           ptx::mma_commit_elect(bar(B_VEMPTY + sv));
-          if (lane == 0 && j == u.n - 1) TRACE2(22, ucnt);
+          if (lane == 0 && j == cu.n - 1) TRACE2(22, ucnt);
         }
-        it += u.n;
+        it += cu.n;
+        if (nxt_id < 0) nxt_id = unit_at(ucnt + 1, true, nu);
+        cu = nu;
+        cur_id = nxt_id;
+        ++ucnt;
+        q_issued = nq;
+        q_ready = nq_ready;
       }
     }
     __syncwarp();
@@ -658,10 +703,9 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
     const float sl2 = plan.scale_log2;
     int sc = 0, oc = 0;
     for (int i = 0;; ++i) {
-      const int unit = unit_at(i, true);
-      if (unit >= plan.total_units) break;
       Unit u;
-      decode_unit(plan, rs, unit, u, dcur);
+      const int unit = unit_at(i, true, u);
+      if (unit >= plan.total_units) break;
       if (wg == 1 && !u.tile1) continue;
       const int origin = wg ? u.origin1 : u.origin0;
       const bool sc_on = (wg ? u.sc1 : u.sc0) && scores != nullptr;
@@ -819,10 +863,9 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
     int selc = 0;
     (void)selc;
     for (int i = 0;; ++i) {
-      const int unit = unit_at(i, true);
-      if (unit >= plan.total_units) break;
       Unit u;
-      decode_unit(plan, rs, unit, u, dcur);
+      const int unit = unit_at(i, true, u);
+      if (unit >= plan.total_units) break;
       for (int i = 0; i < (u.tile1 ? 2 : 1); ++i) {
         const uint32_t tO = tmem + lane_off + tmem_o(i);
         ptx::mbar_wait(bar(B_OFULL + i), oc[i] & 1);

@@ -42,24 +42,19 @@ bound = [g[i] for i in range(len(g)) if (i + 1) % n_unit == 0]
 print(f"steps/unit {n_unit}: median inner period {np.median(inner):.0f}, median boundary gap {np.median(bound):.0f}, "
       f"boundary overhead per unit {np.median(bound) - np.median(inner):.0f} clk = "
       f"{(np.median(bound) - np.median(inner)) / (n_unit * np.median(inner)) * 100:.1f}% of a unit")
-# unit boundary anatomy (softmax WG0): last P of unit u -> O_full wait start/end -> epilogue end -> first S of u+1
-for u_ in range(1, 4):
-    lastP = tr[4, u_ * n_unit - 1]; ow0 = tr[14, 2 * (u_ - 1)]; ow1 = tr[14, 2 * (u_ - 1) + 1]
-    ep_end = tr[14, 256 + u_]; firstS = tr[2, u_ * n_unit]; firstS_wait = tr[0, u_ * n_unit]
-    print(f"unit {u_-1}->{u_}: lastP->Ofull wait done {ow1 - lastP}, epilogue {ep_end - ow1}, "
-          f"epilogue end->next S ready {firstS - ep_end}; MMA: last PV0 issue {tr[7, u_*n_unit-1]-lastP} after lastP, "
-          f"first V wait of next unit at {tr[10, u_*n_unit] - lastP}, got {tr[11, u_*n_unit] - lastP}")
-
-for u_ in range(1, 4):
-    lastP = tr[4, u_ * n_unit - 1]
-    print(f"unit {u_}: producer q_empty wait {tr[20,u_]-lastP}..{tr[21,u_]-lastP}; MMA Q wait {tr[16,u_]-lastP}..{tr[17,u_]-lastP}; "
-          f"K0 at {tr[18,u_]-lastP}, K1 at {tr[19,u_]-lastP} (relative to last P of unit {u_-1})")
+# unit boundary anatomy, relative to the last P of softmax WG0 in unit u-1 (clk)
+for u_ in range(1, 7):
+    e = u_ * n_unit - 1
+    lastP = tr[4, e]
+    r = lambda k, i: int(tr[k, i] - lastP)
+    print(f"boundary {u_}: P1last {r(5, e)}; MMA gotP0 {r(7, e)} gotP1 {r(9, e)} unit-end {r(22, u_ - 1)} "
+          f"decode {r(23, 2 * u_)}..{r(23, 2 * u_ + 1)} Qwait {r(16, u_)}..{r(17, u_)} K0 {r(18, u_)} K1 {r(19, u_)}; "
+          f"Qprod QEMPTY wait {r(20, u_)}..{r(21, u_)}; sm0 waitS' {r(0, e + 1)} gotS' {r(2, e + 1)} P' {r(4, e + 1)} "
+          f"gotS'1 {r(2, e + 2)}; sm1 gotS' {r(3, e + 1)}")
 print("rows around the first boundary (absolute, minus t0):")
 print("iter " + " ".join(f"{n:>8s}" for n in names))
 for i in range(n_unit - 3, n_unit + 3):
     print(f"{i:4d} " + " ".join(f"{(tr[k, i] - t0):8d}" for k in range(14)))
-print("WG1 epilogue O-wait", tr[15, 0] - t0, tr[15, 1] - t0, "end", tr[15, 257] - t0)
-print("WG0 epilogue O-wait", tr[14, 0] - t0, tr[14, 1] - t0, "end", tr[14, 257] - t0)
 print("MMA unit1 Qwait", tr[16, 1] - t0, tr[17, 1] - t0, "K0", tr[18, 1] - t0, "K1", tr[19, 1] - t0)
 print("MMA end of unit0 (after last commit)", tr[22, 0] - t0, " unit1 decode start/end", tr[23, 2] - t0, tr[23, 3] - t0)
 
