@@ -490,6 +490,44 @@ def reuse_in_stream(st, reps=BLOCK_CYCLE_REUSE, iters=5):
     return statistics.median(ts)
 
 
+def select_in_stream(st, reps=BLOCK_CYCLE_REUSE, iters=5):
+    """Select per-launch time in a stream: one CUDA graph of `reps` back-to-back
+    launches over the step's own raw scores (L2-resident after the first launch, as
+    when select directly follows the Refresh that wrote them), so launch latency
+    overlaps the previous launch (PDL) -- the event-timed floor of one launch on
+    this box is ~5-6 us (profiles/r02_flush_modes.log: an empty fill)."""
+    import torch
+    lib, dev = st.lib, st.dev
+    pc = st.pieces[0]
+    sel = lib.select_groups if st.select == "groups" else lib.select_heads
+    cs = torch.cuda.Stream(dev)
+
+    def launches():
+        for _ in range(reps):
+            sel(pc["p"], pc["buf"].scores, pc["buf"].idx, cs)
+
+    cs.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(cs):
+        launches()
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cs):
+        launches()
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    ts = []
+    stream = torch.cuda.current_stream(dev)
+    for it in range(iters + 2):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if it >= 2:
+            ts.append(e0.elapsed_time(e1) * 1e-3 / reps)
+    return statistics.median(ts)
+
+
 def lm_head_result(dev, lib, synth, tf_peak, iters=10):
     """N4: dllm_lm_head_argmax at the LLaDA-8B LM head (2,048 x 4,096 x 126,464)."""
     import torch
@@ -518,7 +556,7 @@ def lm_head_result(dev, lib, synth, tf_peak, iters=10):
             "note": "weight (1.04 GB) larger than L2: no flush needed"}
 
 
-def kernels_result(st, t_ref, t_sel, t_reu, tf_peak, hbm_peak, reuse_stream_s=None):
+def kernels_result(st, t_ref, t_sel, t_reu, tf_peak, hbm_peak, reuse_stream_s=None, select_stream_s=None):
     flops, reuse_u, reuse_l, sel = st.algorithmic()
     m = statistics.mean
     if st.mixed:
@@ -550,6 +588,12 @@ def kernels_result(st, t_ref, t_sel, t_reu, tf_peak, hbm_peak, reuse_stream_s=No
             "in_stream_timing": f"CUDA graph of {BLOCK_CYCLE_REUSE} back-to-back launches over 3 rotating input "
                                 "sets (no L2 reuse), graph time / launches"})
         out["block_cycle_us_in_stream"] = 1e6 * (m(t_ref) + m(t_sel) + BLOCK_CYCLE_REUSE * reuse_stream_s)
+    if select_stream_s is not None:
+        out["select"].update({
+            "us_in_stream": 1e6 * select_stream_s, "GB/s_in_stream": sel / select_stream_s / 1e9,
+            "in_stream_timing": f"CUDA graph of {BLOCK_CYCLE_REUSE} back-to-back launches over the step's scores "
+                                "(L2-resident after the first, as after the Refresh that writes them), graph time / "
+                                "launches; a single event-timed launch carries a ~5-6 us floor on this box"})
     return out, flops, reuse_u
 
 
@@ -561,7 +605,8 @@ def config_result(cfg_name, dev, lib, synth, shard, tf_peak, hbm_peak, steps, wa
     g = capture_graph(st)
     total = time_graph(st, g, steps, warmup, flush)
     rs = None if st.mixed else reuse_in_stream(st)
-    kern, flops, reuse_u = kernels_result(st, t_ref, t_sel, t_reu, tf_peak, hbm_peak, rs)
+    ss = None if st.mixed else select_in_stream(st)
+    kern, flops, reuse_u = kernels_result(st, t_ref, t_sel, t_reu, tf_peak, hbm_peak, rs, ss)
     del g
     return {"workload": workload_desc(wl, 1, "weak") + ("" if select == "heads" else
                                                        ", selection: one set per KV group (dllm_select_groups),"
@@ -627,8 +672,10 @@ def main():
     total_max = float(tt.item())
     reqs_per_step = glob.num_requests
     value = reqs_per_step * args.steps / total_max
-    rs = reuse_in_stream(st) if (rank == 0 and world == 1 and not st.mixed and not args.no_in_stream) else None
-    kern, flops, reuse_u = kernels_result(st, t_ref, t_sel, t_reu, tf_peak, hbm_peak, rs)
+    in_stream = rank == 0 and world == 1 and not st.mixed and not args.no_in_stream
+    rs = reuse_in_stream(st) if in_stream else None
+    ss = select_in_stream(st) if in_stream else None
+    kern, flops, reuse_u = kernels_result(st, t_ref, t_sel, t_reu, tf_peak, hbm_peak, rs, ss)
 
     # ---- multi-GPU: all-gather of the per-request outputs (serial and overlapped)
     gather = None

@@ -27,7 +27,8 @@ namespace dllm {
 #endif
 constexpr int kSelThreads = DLLM_SEL_THREADS;
 constexpr int kSelWarps = kSelThreads / 32;
-constexpr int kSelSmemMaxWords = 32772;   // DLLM_MAX_SELECT_LEN raw scores (+ alignment slack)
+constexpr int kSelSmemMaxWords = 32772;
+constexpr int kSelCollect = 32;   // threshold-bin size finished by one warp (select_heads_kernel)   // DLLM_MAX_SELECT_LEN raw scores (+ alignment slack)
 #ifdef DLLM_TRACE
 // dev: phase timestamps (clock64) of a few CTAs: [cta][0 start, 1 after wait, 2 request found,
 // 3 raw staged, 4 pooled, 5..8 radix passes, 9 compaction done]
@@ -122,10 +123,12 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
   __shared__ int warp_buf[32];
   __shared__ uint32_t s_prefix;
   __shared__ int s_krem;
+  __shared__ int s_ncand, s_nbin;
+  __shared__ uint32_t s_cand[kSelCollect];
 
   SEL_TR(0);
-  pdl_wait_then_trigger();
-  SEL_TR(1);
+  // the request lookup reads only the launch plan: done before griddepcontrol.wait,
+  // so with PDL it overlaps the producing kernel's tail (~450 clk of parameter loads)
   const int T = blockDim.x, tid = threadIdx.x;
   const int b = blockIdx.x / plan.H;
   const int h = blockIdx.x - b * plan.H;
@@ -133,10 +136,13 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
   const int L = R.L, bs = R.bs, blk = R.be - R.bs;
   const int n = L - blk;
   const int k = R.k;
-  if (k <= 0) return;
   const float *raw = scores + R.score_off + (int64_t)h * L;
   int32_t *out = idx + R.idx_off + (int64_t)h * k;
   const int half = plan.window >> 1;
+  if (tid == 0) s_ncand = 0;
+  SEL_TR(1);
+  pdl_wait_then_trigger();
+  if (k <= 0) return;
   SEL_TR(2);
 
   // 1. stage the raw scores (coalesced), then every thread pools its own E
@@ -193,10 +199,50 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
   // buffered histogram saving one barrier per pass: C1 13.3 -> 13.3 us, C4 138 -> 152.)
   uint32_t prefix = 0u, mask = 0u;
   int krem = k;
+  int nbin = n;   // keys that share the current prefix
 #pragma unroll 1
   for (int shift = 24; shift >= 0; shift -= 8) {
+    if (shift < 24 && nbin <= kSelCollect) {
+      // Few keys left in the threshold bin (on realistic scores the common case
+      // after the second digit): collect them and finish with one warp instead of two more radix
+      // passes (~1,300 clk each, mostly barriers).  Every key above the bin is
+      // selected; among the bin's nbin keys the krem-th largest key is the threshold
+      // -- the same threshold and the same tie rule as the full radix select.
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (c0 + e < n && (key[e] & mask) == prefix) s_cand[atomicAdd(&s_ncand, 1)] = key[e];
+      __syncthreads();
+      if (tid < 32) {
+        const uint32_t mine = tid < nbin ? s_cand[tid] : 0u;
+        int gt = 0, ge = 0;
+#pragma unroll
+        for (int j = 0; j < kSelCollect; ++j) {
+          const uint32_t o = __shfl_sync(0xffffffffu, mine, j);   // register rank, no smem chain
+          gt += j < nbin && o > mine;
+          ge += j < nbin && o >= mine;
+        }
+        // the lane whose key has fewer than krem keys above it and at least krem at
+        // or above it holds the threshold (all such lanes hold the same key)
+        const bool hit = tid < nbin && gt < krem && krem <= ge;
+        const uint32_t who = __ballot_sync(0xffffffffu, hit);
+        const int src = __ffs(who) - 1;
+        const uint32_t thr_key = __shfl_sync(0xffffffffu, mine, src);
+        const int gt_thr = __shfl_sync(0xffffffffu, gt, src);
+        if (tid == 0) {
+          s_prefix = thr_key;
+          s_krem = krem - gt_thr;   // keys equal to the threshold still needed
+        }
+      }
+      __syncthreads();
+      prefix = s_prefix;
+      krem = s_krem;
+      SEL_TR(5 + (24 - shift) / 8);
+      break;
+    }
     for (int i = tid; i < 256; i += T) hist[i] = 0;
     __syncthreads();
+    // (warp-aggregated atomics via match.any for the crowded first digit were
+    // measured slower: C1 pass 2,500 vs 1,900 clk, C4 6,300-7,300 vs 3,000-4,400)
 #pragma unroll
     for (int e = 0; e < E; ++e)
       if (c0 + e < n && (key[e] & mask) == prefix) atomicAdd(&hist[(key[e] >> shift) & 0xffu], 1);
@@ -222,6 +268,7 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
           if (acc + cnt[i] >= krem) {
             s_prefix = prefix | ((uint32_t)(base + 7 - i) << shift);
             s_krem = krem - acc;
+            s_nbin = cnt[i];      // keys in the chosen bin
             break;
           }
           acc += cnt[i];
@@ -231,6 +278,7 @@ select_heads_kernel(const __grid_constant__ Plan plan, const float *__restrict__
     __syncthreads();
     prefix = s_prefix;
     krem = s_krem;
+    nbin = s_nbin;
     mask |= 0xffu << shift;
     SEL_TR(5 + (24 - shift) / 8);
   }
