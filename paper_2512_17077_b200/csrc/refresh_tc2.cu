@@ -165,27 +165,66 @@ struct Unit {
 // head, Q-tile pair and importance-epilogue flags.  Called once per unit by the
 // K/V producer only; the other roles receive the decoded Unit through shared memory.
 __device__ __forceinline__ void decode_unit(const Plan &pl, const ReqInfo *rs, int unit, Unit &u) {
-  int lo = 0, hi = pl.nreq - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (rs[mid].unit_off <= unit) lo = mid; else hi = mid - 1;
+  // Unit order (the order in which the CTAs claim them).  With the importance
+  // epilogue, the H * nreq pairs that carry it (the pair holding the active block's
+  // tile, one per (request, head); their softmax warpgroup also reduces the block
+  // rows' column maxima every step) come FIRST, the plain pairs after them: the
+  // longest units are dealt first, so the last units of the launch -- which set
+  // the tail of the dynamically scheduled grid -- are the short ones (LPT).
+  int b, h, p;
+  const ReqInfo *R;
+  int nreg, ntiles, npairs;
+  bool extra;
+  auto shape = [&](const ReqInfo &r) {
+    nreg = regular_tiles(r.L);
+    extra = pl.with_scores && straddles(r.bs, r.be);
+    ntiles = nreg + (extra ? 1 : 0);
+    npairs = (ntiles + 1) >> 1;
+  };
+  if (pl.with_scores) {
+    const int n_imp = pl.nreq * pl.H;
+    if (unit < n_imp) {
+      b = unit / pl.H;
+      h = unit - b * pl.H;
+      R = &rs[b];
+      shape(*R);
+      p = (extra ? nreg : R->bs / TBM) >> 1;
+    } else {
+      // plain pairs: request b owns [unit_off(b) - b H, unit_off(b + 1) - (b + 1) H)
+      const int v = unit - n_imp;
+      int lo = 0, hi = pl.nreq - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (rs[mid].unit_off - mid * pl.H <= v) lo = mid; else hi = mid - 1;
+      }
+      b = lo;
+      R = &rs[b];
+      shape(*R);
+      const int np1 = npairs - 1;
+      const int local = v - (R->unit_off - b * pl.H);
+      h = local / np1;
+      const int q = local - h * np1;
+      const int p_imp = (extra ? nreg : R->bs / TBM) >> 1;
+      p = q < p_imp ? q : q + 1;
+    }
+  } else {
+    int lo = 0, hi = pl.nreq - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (rs[mid].unit_off <= unit) lo = mid; else hi = mid - 1;
+    }
+    b = lo;
+    R = &rs[b];
+    shape(*R);
+    const int local = unit - R->unit_off;
+    h = local / npairs;
+    p = local - h * npairs;
   }
-  const ReqInfo &R = rs[lo];
-  u.L = R.L; u.bs = R.bs; u.be = R.be;
-  u.q_off = R.q_off; u.bt_row = R.bt_row; u.score_off = R.score_off;
-  u.k = R.k; u.idx_off = R.idx_off;
-  const int nreg = regular_tiles(u.L);
-  const bool extra = pl.with_scores && straddles(u.bs, u.be);
-  const int ntiles = nreg + (extra ? 1 : 0);
-  const int npairs = (ntiles + 1) >> 1;
-  const int local = unit - R.unit_off;
-  u.h = local / npairs;
-  // tile pairs are rotated by head: units are dealt to CTAs with a stride of
-  // gridDim.x (a multiple of 4 on B200), so without the rotation one CTA in
-  // npairs would always get the pair that holds the active block, and with it
-  // all of the importance-epilogue work (a 30% longer critical path)
-  const int p = (local - u.h * npairs + u.h) % npairs;
-  u.kvh = u.h / (pl.H / pl.H_kv);
+  u.L = R->L; u.bs = R->bs; u.be = R->be;
+  u.q_off = R->q_off; u.bt_row = R->bt_row; u.score_off = R->score_off;
+  u.k = R->k; u.idx_off = R->idx_off;
+  u.h = h;
+  u.kvh = h / (pl.H / pl.H_kv);
   u.n = (u.L + TBN - 1) / TBN;
   const int t0 = 2 * p, t1 = 2 * p + 1;
   u.tile1 = t1 < ntiles;
