@@ -1024,7 +1024,7 @@ mixed_tc_kernel(const __grid_constant__ Plan rplan, const __grid_constant__ CUte
     refresh_tc2_body<128>(rplan, tm_q, tm_k, tm_v, tm_o, out, scores, sel_idx, (int)blockIdx.x, n_ref);
   } else {
     // (griddepcontrol.wait inside the body, after its input-independent prologue)
-    rtc::reuse_tc_body(uplan, q_blk, k_cache, v_cache, idx, out_blk, (int)blockIdx.x - n_ref, (int)gridDim.x - n_ref);
+    rtc::reuse_tc_body<128>(uplan, q_blk, k_cache, v_cache, idx, out_blk, (int)blockIdx.x - n_ref, (int)gridDim.x - n_ref);
   }
 }
 static_assert(THREADS == rtc::kTThreads, "mixed kernel: both bodies run 512-thread CTAs");

@@ -21,12 +21,13 @@ namespace {
 
 using namespace rtc;
 
+template <int DP>
 __global__ void __launch_bounds__(kTThreads, 1)
 reuse_tc_kernel(const __grid_constant__ Plan plan, const __nv_bfloat16 *__restrict__ q_blk,
                 const __nv_bfloat16 *__restrict__ k_cache, const __nv_bfloat16 *__restrict__ v_cache,
                 const int32_t *__restrict__ idx, __nv_bfloat16 *__restrict__ out) {
   // (griddepcontrol.wait inside the body, after the input-independent prologue)
-  reuse_tc_body(plan, q_blk, k_cache, v_cache, idx, out, (int)blockIdx.x, (int)gridDim.x);
+  reuse_tc_body<DP>(plan, q_blk, k_cache, v_cache, idx, out, (int)blockIdx.x, (int)gridDim.x);
 }
 
 int num_sms_tc() {
@@ -42,28 +43,36 @@ int num_sms_tc() {
 
 }  // namespace
 
-bool reuse_tc_supported(int D) { return D == kTD; }
+// D = 128 on the 128-dim layout; D = 16, 32, 64 on the 64-dim layout (zero-padded rows)
+bool reuse_tc_supported(int D) { return D == 128 || D == 64 || D == 32 || D == 16; }
 
 // CTAs for a Reuse plan: one per SM (persistent), at most one per unit
 int reuse_tc_grid(const Plan &plan, int max_ctas) {
   return plan.total_units < max_ctas ? plan.total_units : max_ctas;
 }
 
-cudaError_t launch_reuse_tc(const Plan &plan, const void *q_blk, const void *k_cache, const void *v_cache,
-                            const int32_t *idx, void *out, void *workspace, cudaStream_t st) {
-  (void)workspace;
-  if (plan.D != kTD) return cudaErrorInvalidValue;
+template <int DP>
+cudaError_t launch_dp(const Plan &plan, const void *q_blk, const void *k_cache, const void *v_cache,
+                      const int32_t *idx, void *out, cudaStream_t st) {
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
   std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(reuse_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTBytes);
+    attr = cudaFuncSetAttribute(reuse_tc_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, RL<DP>::kBytes);
   });
   if (attr != cudaSuccess) return attr;
   const int grid = reuse_tc_grid(plan, num_sms_tc());
   if (grid <= 0) return cudaSuccess;
-  return launch_pdl(reuse_tc_kernel, dim3(grid), dim3(kTThreads), (size_t)kTBytes, st, plan,
+  return launch_pdl(reuse_tc_kernel<DP>, dim3(grid), dim3(kTThreads), (size_t)RL<DP>::kBytes, st, plan,
                     (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k_cache, (const __nv_bfloat16 *)v_cache, idx,
                     (__nv_bfloat16 *)out);
+}
+
+cudaError_t launch_reuse_tc(const Plan &plan, const void *q_blk, const void *k_cache, const void *v_cache,
+                            const int32_t *idx, void *out, void *workspace, cudaStream_t st) {
+  (void)workspace;
+  if (!reuse_tc_supported(plan.D)) return cudaErrorInvalidValue;
+  return plan.D == 128 ? launch_dp<128>(plan, q_blk, k_cache, v_cache, idx, out, st)
+                       : launch_dp<64>(plan, q_blk, k_cache, v_cache, idx, out, st);
 }
 
 }  // namespace dllm

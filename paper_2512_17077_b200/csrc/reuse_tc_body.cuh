@@ -46,7 +46,13 @@
 namespace dllm {
 namespace rtc {
 
-constexpr int kTD = 128;            // head dim supported by this kernel
+constexpr int kTD = 128;            // head dim of the default layout (the mixed kernel's)
+// The layout is built for a padded head dim DP in {64, 128}: D = 128 uses DP = 128;
+// D = 16, 32, 64 use DP = 64 -- every row gathered into shared memory is zero-padded
+// to DP dims (the 16-byte pieces past D are cp.async zero-fills), so S^T = K Q^T is
+// unchanged, and O^T = V^T P^T keeps its M = 128 MMA: with DP = 64 its A operand's
+// second 64-dim atom is read from the next 12 KB of shared memory (finite data) into
+// TMEM lanes 64-127, which the epilogue never reads.
 constexpr int kTRows = 32;          // query rows per unit (MMA N)
 #ifndef DLLM_RTC_KEYS
 #define DLLM_RTC_KEYS 96
@@ -75,20 +81,29 @@ __device__ __forceinline__ int loader_index(int w) { return w < 4 ? w : (w == 6 
 constexpr int kTThreads = kTWarps * 32;
 
 // shared memory (offsets from a 1024-byte aligned base)
-constexpr int kTileK = kTChunk * kTD * 2;       // [2 atoms][kTChunk rows][128 B]
-constexpr int kStage = 2 * kTileK;              // K then V
-constexpr int kQTile = kTRows * kTD * 2;        // 8 KB: [2 atoms][32 rows][128 B]
-constexpr int kOffQ = kTNS * kStage;
-constexpr int kOffOffs = kOffQ + 2 * kQTile;    // [kTNT][kTChunk] int32
-constexpr int kOffRed = kOffOffs + kTNT * kTChunk * 4;   // [4 warps][32] chunk row maxima
-constexpr int kOffL = kOffRed + 4 * 32 * 4;            // [2 O buffers][4 warps][32 rows] partial row sums
-constexpr int kOffStage = kOffL + 2 * 4 * 32 * 4;      // output staging [32 rows][D] bf16
 constexpr int kBtMax = 1024;                          // block-table entries cached in shared memory
-constexpr int kOffBt = kOffStage + kTRows * kTD * 2;  // [kBtMax] int32
-constexpr int kOffBar = kOffBt + kBtMax * 4;
 constexpr int kNumBars = 2 * kTNS + 2 * kTNT + 2 + 2 + 2 + 2 + 2 + 1 + 2 + 2 + 2 + 1;
-constexpr int kTBytes = kOffBar + 8 * kNumBars + 1024;   // + alignment slack
-static_assert(kTBytes <= 227 * 1024, "reuse_tc shared memory");
+template <int DP>
+struct RL {
+  static constexpr int kTileK = kTChunk * DP * 2;          // [DP/64 atoms][kTChunk rows][128 B]
+  static constexpr int kStage = 2 * kTileK;                // K then V
+  static constexpr int kQTile = kTRows * DP * 2;           // [DP/64 atoms][32 rows][128 B]
+  static constexpr int kOffQ = kTNS * kStage;
+  static constexpr int kOffOffs = kOffQ + 2 * kQTile;      // [kTNT][kTChunk] int32
+  static constexpr int kOffRed = kOffOffs + kTNT * kTChunk * 4;   // [4 warps][32] chunk row maxima
+  static constexpr int kOffL = kOffRed + 4 * 32 * 4;              // [2 O buffers][4 warps][32 rows] partial row sums
+  static constexpr int kOffStage = kOffL + 2 * 4 * 32 * 4;        // output staging [32 rows][D] bf16
+  static constexpr int kOffBt = kOffStage + kTRows * DP * 2;      // [kBtMax] int32
+  static constexpr int kOffBar = kOffBt + kBtMax * 4;
+  static constexpr int kBytes = kOffBar + 8 * kNumBars + 1024;    // + alignment slack
+  static_assert(kBytes <= 227 * 1024, "reuse_tc shared memory");
+  // the O^T MMA with DP = 64 reads a second 64-dim atom kTChunk * 128 bytes past each
+  // stage's V tile: still inside the allocation (the next stage, or the Q tiles and
+  // the offset ring after the last one).  Whatever it reads (NaN bit patterns
+  // included) only reaches accumulator rows 64-127, which are never read.
+  static_assert(DP == 128 || kTNS * kStage + kTChunk * 128 <= kOffBar, "reuse_tc DP = 64 overread");
+};
+constexpr int kTBytes = RL<kTD>::kBytes;
 
 // TMEM columns: S^T double buffer (32 each), O^T double buffer (32 each)
 constexpr uint32_t kTmemCols = 128;
@@ -178,12 +193,15 @@ __device__ __forceinline__ float transpose_reduce32(float (&x)[32], int lane) {
 // single-launch mixed Refresh/Reuse kernel (refresh_tc2.cu): CTA `cta` of `ncta`
 // CTAs working on this plan.  It executes griddepcontrol.wait itself, after its
 // input-independent prologue: the caller must not read global memory before.
+template <int DP>
 __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloat16 *__restrict__ q_blk,
                                               const __nv_bfloat16 *__restrict__ k_cache,
                                               const __nv_bfloat16 *__restrict__ v_cache,
                                               const int32_t *__restrict__ idx, __nv_bfloat16 *__restrict__ out,
                                               const int cta, const int ncta) {
-  constexpr int D = kTD;
+  using Lc = RL<DP>;
+  constexpr int D = DP;        // padded head dim of the shared-memory layout and the MMAs
+  const int Dg = DP == kTD ? kTD : plan.D;   // head dim of the tensors in global memory (<= DP)
   constexpr int CH = D / 8;    // 16-byte pieces per row
   constexpr int NS = kTNS;
   extern __shared__ uint8_t smem_raw[];
@@ -193,7 +211,7 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // barriers
-  const uint32_t b_kvfull = sb + kOffBar;             // [NS] loaders (32*kTLoaders noinc)
+  const uint32_t b_kvfull = sb + Lc::kOffBar;             // [NS] loaders (32*kTLoaders noinc)
   const uint32_t b_kvempty = b_kvfull + 8 * NS;       // [NS] MMA commit
   const uint32_t b_ofull_t = b_kvempty + 8 * NS;      // [kTNT] translator (1)
   const uint32_t b_oempty_t = b_ofull_t + 8 * kTNT;   // [kTNT] loaders (kTLoaders)
@@ -210,7 +228,7 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
   // i-th unit of this CTA (static round-robin; a device-counter scheduler measured
   // 5-8% slower here, profiles/r01_ab_reuse_dynsched_qprefetch.log)
   auto unit_at = [&](int i) -> int { return cta + i * ncta; };
-  int32_t *offs = reinterpret_cast<int32_t *>(gb + kOffOffs);
+  int32_t *offs = reinterpret_cast<int32_t *>(gb + Lc::kOffOffs);
 
 #ifdef DLLM_TRACE
   if (threadIdx.x == 0 && cta < 1024) {
@@ -260,7 +278,7 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
   if (warp == kTransWarp) {
     // ============================ translator (+ Q rows) ============================
     int t = 0, bt_cached = -1;
-    int *bts = reinterpret_cast<int *>(gb + kOffBt);
+    int *bts = reinterpret_cast<int *>(gb + Lc::kOffBt);
     int unit = cta;
     for (int i = 0;; ++i) {
       if (unit >= plan.total_units) break;
@@ -347,7 +365,7 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
   } else if (loader_index(warp) >= 0) {
     // ============================ loaders ============================
     const int li = loader_index(warp);
-    const int64_t HD = (int64_t)plan.H * D;
+    const int64_t HD = (int64_t)plan.H * Dg;
     int t = 0, qc = 0;
     for (int i = 0;; ++i, ++qc) {
       const int unit = unit_at(i);
@@ -360,11 +378,12 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
         const int row0 = u.rg * kTRows;
         const int qb = qc & 1;
         ptx::mbar_wait(b_qempty + 8 * qb, ((qc >> 1) & 1) ^ 1);
-        const uint32_t sq = sb + kOffQ + qb * kQTile;
+        const uint32_t sq = sb + Lc::kOffQ + qb * Lc::kQTile;
         for (int i = li * 32 + lane; i < kTRows * CH; i += 32 * kTLoaders) {
           const int r = i / CH, c = i - r * CH;
-          const bool ok = row0 + r < u.blk;
-          const __nv_bfloat16 *src = q_blk + (int64_t)(u.blk_off + (ok ? row0 + r : 0)) * HD + (int64_t)u.h * D + c * 8;
+          // rows past the block and (DP = 64) dims past D: zeros
+          const bool ok = row0 + r < u.blk && (D == kTD || c * 8 < Dg);
+          const __nv_bfloat16 *src = q_blk + (int64_t)(u.blk_off + (ok ? row0 + r : 0)) * HD + (int64_t)u.h * Dg + c * 8;
           cp_async16(sq + sw128_off(kTRows, r, c), src, ok ? 16 : 0);
         }
         cp_async_arrive_noinc(b_qfull + 8 * qb);
@@ -373,13 +392,14 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
         const int slot = t % kTNT, s = t % NS;
         ptx::mbar_wait(b_ofull_t + 8 * slot, (t / kTNT) & 1);
         ptx::mbar_wait(b_kvempty + 8 * s, ((t / NS) & 1) ^ 1);
-        const uint32_t dk = sb + s * kStage, dv = dk + kTileK;
+        const uint32_t dk = sb + s * Lc::kStage, dv = dk + Lc::kTileK;
 #pragma unroll 4
         for (int e = li * 32 + lane; e < kTChunk * CH; e += 32 * kTLoaders) {
           const int r = e / CH, cc = e - r * CH;
           const int off = offs[slot * kTChunk + r];
-          const int64_t goff = (int64_t)(off < 0 ? 0 : off) * D + cc * 8;
-          const int nb = off < 0 ? 0 : 16;
+          const bool ok = off >= 0 && (D == Dg || cc * 8 < Dg);
+          const int64_t goff = ok ? (int64_t)off * Dg + cc * 8 : 0;
+          const int nb = ok ? 16 : 0;
           const uint32_t so = sw128_off(kTChunk, r, cc);
           cp_async16(dk + so, k_cache + goff, nb);
           cp_async16(dv + so, v_cache + goff, nb);
@@ -396,8 +416,8 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
     constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(128, kTRows, false, false);
     constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(128, kTRows, true, true);
     const uint64_t dk0 = ptx::smem_desc_sw128(sb, 16, 1024);                 // K tile (K-major) / P^T (K-major)
-    const uint64_t dv0 = ptx::smem_desc_sw128(sb + kTileK, kTChunk * 128, 1024);   // V tile as MN-major A
-    const uint64_t dq0 = ptx::smem_desc_sw128(sb + kOffQ, 16, 1024);
+    const uint64_t dv0 = ptx::smem_desc_sw128(sb + Lc::kTileK, kTChunk * 128, 1024);   // V tile as MN-major A
+    const uint64_t dq0 = ptx::smem_desc_sw128(sb + Lc::kOffQ, 16, 1024);
     // P^T MN-major SW64: one 32-row atom along N, 8-key groups 512 B apart along K
     const uint64_t dpm0 = ptx::smem_desc(sb, 64 * 8 * 2, 512, ptx::kSwizzle64B);
     int t = 0, uc = 0;
@@ -406,8 +426,8 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
       ptx::mbar_wait(b_pfull + 8 * (pv_t & 1), (pv_t >> 1) & 1);
       if (pv_first) ptx::mbar_wait(b_ofree + 8 * pv_ob, ((pv_uc >> 1) & 1) ^ 1);
       ptx::tc_fence_after();
-      const uint64_t a0 = dv0 + (uint64_t)((pv_s * kStage) >> 4);
-      const uint64_t p0 = dpm0 + (uint64_t)((pv_s * kStage) >> 4);
+      const uint64_t a0 = dv0 + (uint64_t)((pv_s * Lc::kStage) >> 4);
+      const uint64_t p0 = dpm0 + (uint64_t)((pv_s * Lc::kStage) >> 4);
 #pragma unroll
       for (int k = 0; k < kTChunk / 16; ++k) {
         const uint32_t ao = (uint32_t)((k * 16 * 128) >> 4);
@@ -443,8 +463,8 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
         ptx::mbar_wait(b_sfree + 8 * sbuf, ((t >> 1) & 1) ^ 1);
         ptx::fence_proxy_async_smem();   // cp.async (generic proxy) data -> tensor core (async proxy)
         ptx::tc_fence_after();
-        const uint64_t a0 = dk0 + (uint64_t)((s * kStage) >> 4);
-        const uint64_t b0 = dq0 + (uint64_t)((qb * kQTile) >> 4);
+        const uint64_t a0 = dk0 + (uint64_t)((s * Lc::kStage) >> 4);
+        const uint64_t b0 = dq0 + (uint64_t)((qb * Lc::kQTile) >> 4);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t ao = (uint32_t)(((k >> 2) * kTChunk * 128 + (k & 3) * 32) >> 4);
@@ -475,8 +495,8 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
     asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n" ::: "memory");
     const int sw = warp & 3;   // TMEM lane quarter
     const float sl2 = plan.scale_log2;
-    float *red = reinterpret_cast<float *>(gb + kOffRed);   // [4 warps][32] chunk maxima
-    float *lbuf = reinterpret_cast<float *>(gb + kOffL);
+    float *red = reinterpret_cast<float *>(gb + Lc::kOffRed);   // [4 warps][32] chunk maxima
+    float *lbuf = reinterpret_cast<float *>(gb + Lc::kOffL);
     const uint32_t lane_base = (uint32_t)(sw * 32) << 16;
     int t = 0, uc = 0;
     for (int i = 0;; ++i, ++uc) {
@@ -563,7 +583,7 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
         // P^T over the stage's K tile, MN-major SW64 operand: key kc's 32 row values are
         // one 64-byte row (4 pieces of 16 B), piece j stored at j ^ ((kc >> 1) & 3)
         const int kc = sw * 32 + lane;
-        uint8_t *prow = gb + (t % NS) * kStage + kc * 64;
+        uint8_t *prow = gb + (t % NS) * Lc::kStage + kc * 64;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           uint32_t w4[4];
@@ -600,7 +620,7 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
     asm volatile("setmaxnreg.inc.sync.aligned.u32 152;\n" ::: "memory");
     const int ew = warp & 3;
     const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
-    const float *lbuf = reinterpret_cast<const float *>(gb + kOffL);
+    const float *lbuf = reinterpret_cast<const float *>(gb + Lc::kOffL);
     int uc = 0;
     for (int i = 0;; ++i, ++uc) {
       const int unit = unit_at(i);
@@ -623,18 +643,21 @@ __device__ __forceinline__ void reuse_tc_body(const Plan &plan, const __nv_bfloa
       if (lane == 0) ptx::mbar_arrive(b_ofree + 8 * ob);
       if (ew == 0) ptx::bulk_wait_group_read0();   // previous unit's rows left the staging tile
       ptx::named_bar_sync(2, 128);
-      uint8_t *stg = gb + kOffStage + (ew * 32 + lane) * 2;
+      // thread = head dim d (TMEM lane); rows of Dg dims in the staging tile
+      const int d = ew * 32 + lane;
+      uint8_t *stg = gb + Lc::kOffStage + d * 2;
 #pragma unroll
-      for (int n = 0; n < 32; ++n)
-        *reinterpret_cast<__nv_bfloat16 *>(stg + n * (D * 2)) =
-            __float2bfloat16_rn(__uint_as_float(o[n]) * __shfl_sync(0xffffffffu, inv, n));
+      for (int n = 0; n < 32; ++n) {
+        const float v = __uint_as_float(o[n]) * __shfl_sync(0xffffffffu, inv, n);
+        if (D == kTD || d < Dg) *reinterpret_cast<__nv_bfloat16 *>(stg + n * (Dg * 2)) = __float2bfloat16_rn(v);
+      }
       ptx::fence_proxy_async_smem();
       ptx::named_bar_sync(2, 128);
       const int row0 = u.rg * kTRows;
       const int nrows = min(kTRows, u.blk - row0);
       if (ew == 0 && lane < nrows) {
-        ptx::bulk_s2g(out + ((int64_t)(u.blk_off + row0 + lane) * plan.H + u.h) * D, sb + kOffStage + lane * (D * 2),
-                      D * 2);
+        ptx::bulk_s2g(out + ((int64_t)(u.blk_off + row0 + lane) * plan.H + u.h) * Dg,
+                      sb + Lc::kOffStage + lane * (Dg * 2), Dg * 2);
         ptx::bulk_commit_group();
       }
       if (ew == 0) RTC_CHUNK(11, uc);
