@@ -679,8 +679,8 @@ const char *dllm_last_error(void) { return g_last_error.c_str(); }
 
 const char *dllm_version(void) {
   static const std::string v = std::string(
-      "libdllm sm_100a: refresh=tcgen05/TMEM+TMA (mma.sync for D<64), select=radix-topk, "
-      "reuse=paged cp.async gather + tcgen05 (D=128; mma.sync otherwise), mixed=one-launch Refresh+Reuse, "
+      "libdllm sm_100a: refresh=tcgen05/TMEM+TMA (D=16..128), select=radix-topk, "
+      "reuse=paged cp.async gather + tcgen05 (D=16..128), mixed=one-launch Refresh+Reuse, "
       "lm_head=tcgen05 GEMM + fused argmax, select_in_refresh=") + (fused_select_max_n() > 0 ? "on" : "off");
   return v.c_str();
 }

@@ -402,6 +402,10 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
   uint8_t *gb = smem_raw + (sb - raw_u32);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto bar = [&](int i) { return sb + C::kOffBar + 8u * (uint32_t)i; };
+  // head dim of the tensors in global memory: D = 16 and 32 run on the 64-dim layout --
+  // their tensor maps keep 64-column boxes over a Dg-column tensor, so the TMA fills
+  // columns Dg..63 of every row with zeros (out-of-bounds fill) and Q.K^T, P.V are exact
+  const int Dg = D == 128 ? 128 : plan.D;
 
 #ifdef DLLM_TRACE
   if (threadIdx.x == 0 && blockIdx.x < 1024) { g_cta2[blockIdx.x][0] = gtimer(); g_cta2[blockIdx.x][2] = 0; }
@@ -895,7 +899,7 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
     const int wq = warp & 3;
     const int row = wq * 32 + lane;
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    const int64_t HD = (int64_t)plan.H * D;
+    const int64_t HD = (int64_t)plan.H * Dg;
     uint8_t *stg = gb + C::kOffStage + wq * 32 * 64;
     const uint32_t stg_s = sb + C::kOffStage + wq * 32 * 64;
     int oc[2] = {0, 0};
@@ -923,7 +927,7 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
         const int origin = i ? u.origin1 : u.origin0;
         const int wend = i ? u.wend1 : u.wend0;
         const int srow0 = origin + wq * 32;                // first tile row of this warp
-        const bool full_warp = srow0 + 32 <= wend;
+        const bool full_warp = srow0 + 32 <= wend && Dg == D;   // (D < 64: direct stores)
 #pragma unroll
         for (int c = 0; c < D; c += 32) {
           uint32_t pk[16];
@@ -945,10 +949,11 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
               ptx::tma_store_3d(&tm_o, stg_s, c, u.h, u.q_off + srow0);
               ptx::bulk_commit_group();
             }
-          } else if (srow0 + lane < wend) {
-            uint4 *d4 = reinterpret_cast<uint4 *>(out + (int64_t)(u.q_off + srow0 + lane) * HD + (int64_t)u.h * D + c);
+          } else if (srow0 + lane < wend && c < Dg) {
+            uint4 *d4 = reinterpret_cast<uint4 *>(out + (int64_t)(u.q_off + srow0 + lane) * HD + (int64_t)u.h * Dg + c);
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) d4[q4] = make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+            for (int q4 = 0; q4 < 4; ++q4)
+              if (c + 8 * q4 < Dg) d4[q4] = make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
           }
         }
       }
@@ -1053,12 +1058,16 @@ cudaError_t make_maps(const Plan &plan, const void *q, const void *k, const void
                       CUtensorMap &tk, CUtensorMap &tv, CUtensorMap &to) {
   auto enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
+  // Dg <= D: D = 16 / 32 tensors on the 64-dim layout keep the 64-column boxes (the
+  // TMA zero-fills the columns past Dg); their output goes out by direct stores
+  const int Dg = plan.D;
+  const cuuint32_t bq = 64, bo = 32;
   int64_t rows = 0;
   for (int b = 0; b < plan.nreq; ++b) rows = rows > plan.r[b].q_off + plan.r[b].L ? rows : plan.r[b].q_off + plan.r[b].L;
   {
-    cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)plan.H, (cuuint64_t)rows};
-    cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)plan.H * D * 2};
-    cuuint32_t box[3] = {32, 1, 32};
+    cuuint64_t dims[3] = {(cuuint64_t)Dg, (cuuint64_t)plan.H, (cuuint64_t)rows};
+    cuuint64_t strides[2] = {(cuuint64_t)Dg * 2, (cuuint64_t)plan.H * Dg * 2};
+    cuuint32_t box[3] = {bo, 1, 32};
     cuuint32_t es[3] = {1, 1, 1};
     if (enc(&to, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
@@ -1066,9 +1075,9 @@ cudaError_t make_maps(const Plan &plan, const void *q, const void *k, const void
       return cudaErrorInvalidValue;
   }
   {
-    cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)plan.H, (cuuint64_t)rows};
-    cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)plan.H * D * 2};
-    cuuint32_t box[3] = {64, 1, TBM};
+    cuuint64_t dims[3] = {(cuuint64_t)Dg, (cuuint64_t)plan.H, (cuuint64_t)rows};
+    cuuint64_t strides[2] = {(cuuint64_t)Dg * 2, (cuuint64_t)plan.H * Dg * 2};
+    cuuint32_t box[3] = {bq, 1, TBM};
     cuuint32_t es[3] = {1, 1, 1};
     if (enc(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(q), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1077,9 +1086,9 @@ cudaError_t make_maps(const Plan &plan, const void *q, const void *k, const void
   }
   {
     const int P = plan.page_size;
-    cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)P, (cuuint64_t)plan.H_kv, (cuuint64_t)1 << 24};
-    cuuint64_t strides[3] = {(cuuint64_t)D * 2, (cuuint64_t)P * D * 2, (cuuint64_t)plan.H_kv * P * D * 2};
-    cuuint32_t box[4] = {64, (cuuint32_t)(P < TBN ? P : TBN), 1, 1};
+    cuuint64_t dims[4] = {(cuuint64_t)Dg, (cuuint64_t)P, (cuuint64_t)plan.H_kv, (cuuint64_t)1 << 24};
+    cuuint64_t strides[3] = {(cuuint64_t)Dg * 2, (cuuint64_t)P * Dg * 2, (cuuint64_t)plan.H_kv * P * Dg * 2};
+    cuuint32_t box[4] = {bq, (cuuint32_t)(P < TBN ? P : TBN), 1, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     for (int w = 0; w < 2; ++w) {
       if (enc(w ? &tv : &tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(w ? v : k), dims, strides, box,
@@ -1133,7 +1142,8 @@ cudaError_t launch_mixed_tc(const Plan &rplan, const void *q, const void *k, con
 
 int num_sms_mixed() { return num_sms(); }
 
-bool refresh_tc_supported(int D) { return D == 64 || D == 128; }
+// D = 64, 128 on their own layouts; D = 16, 32 on the 64-dim layout (zero-padded rows)
+bool refresh_tc_supported(int D) { return D == 16 || D == 32 || D == 64 || D == 128; }
 
 int fused_select_max_n() { return DLLM_TC2_FUSEDSEL ? kFSelMaxN : 0; }
 
@@ -1145,6 +1155,8 @@ int refresh_tc2_units(int L, int bs, int be, int H, bool with_scores) {
 cudaError_t launch_refresh_tc2(const Plan &plan, const void *q, const void *k, const void *v, void *out,
                                float *scores, int32_t *sel_idx, void *workspace, cudaStream_t st) {
   switch (plan.D) {
+    case 16:
+    case 32:
     case 64: return launch_d<64>(plan, q, k, v, out, scores, sel_idx, workspace, st);
     case 128: return launch_d<128>(plan, q, k, v, out, scores, sel_idx, workspace, st);
   }
