@@ -453,6 +453,12 @@ __device__ __forceinline__ void refresh_tc2_body(const Plan &plan, const CUtenso
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
+  // everything above (barriers, TMEM, tensor-map prefetch) is independent of the
+  // preceding kernel's results: with programmatic dependent launch it overlaps that
+  // kernel's tail; no role touches global memory (inputs, the scheduler counters)
+  // before this wait
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t *>(gb + C::kOffBar + 8 * B_TMEMSLOT);
   // the device counter lives in the caller's workspace (dllm_problem.workspace):
   // without one the units go round-robin
@@ -1004,7 +1010,7 @@ refresh_tc2_kernel(const __grid_constant__ Plan plan, const __grid_constant__ CU
                    const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                    const __grid_constant__ CUtensorMap tm_o, __nv_bfloat16 *__restrict__ out,
                    float *__restrict__ scores, int32_t *__restrict__ sel_idx) {
-  pdl_wait_then_trigger();
+  // (griddepcontrol.wait inside the body, after its input-independent prologue)
   refresh_tc2_body<D>(plan, tm_q, tm_k, tm_v, tm_o, out, scores, sel_idx, (int)blockIdx.x, (int)gridDim.x);
 }
 
@@ -1025,7 +1031,7 @@ mixed_tc_kernel(const __grid_constant__ Plan rplan, const __grid_constant__ CUte
                 const int32_t *__restrict__ idx, __nv_bfloat16 *__restrict__ out_blk, const int n_ref,
                 int32_t *__restrict__ sel_idx) {
   if ((int)blockIdx.x < n_ref) {
-    pdl_wait_then_trigger();
+    // (griddepcontrol.wait inside both bodies, after their input-independent prologues)
     refresh_tc2_body<128>(rplan, tm_q, tm_k, tm_v, tm_o, out, scores, sel_idx, (int)blockIdx.x, n_ref);
   } else {
     // (griddepcontrol.wait inside the body, after its input-independent prologue)
