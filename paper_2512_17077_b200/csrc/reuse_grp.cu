@@ -767,7 +767,8 @@ cudaError_t launch_reuse_grp(const Plan &plan, const void *q_blk, const void *k_
   if (attr != cudaSuccess) return attr;
   // the fewest CTAs that keep the number of static rounds (as reuse_tc_grid)
   const int rounds = (plan.total_units + num_sms() - 1) / num_sms();
-  const int grid = rounds > 0 ? (plan.total_units + rounds - 1) / rounds : 0;
+  const int tail = plan.total_units - (rounds - 1) * num_sms();
+  const int grid = rounds <= 0 ? 0 : (rounds > 1 && 4 * tail < num_sms()) ? num_sms() : (plan.total_units + rounds - 1) / rounds;
   if (grid <= 0) return cudaSuccess;
   return launch_pdl(union_sets ? reuse_grp_kernel<true> : reuse_grp_kernel<false>, dim3(grid), dim3(kThreads),
                     (size_t)kBytes, st, plan, (const __nv_bfloat16 *)q_blk, (const __nv_bfloat16 *)k_cache,

@@ -53,8 +53,13 @@ int reuse_tc_grid(const Plan &plan, int max_ctas) {
   // used at all -- fewer gathers in flight, shorter memory queues: C1 (512 units)
   // runs on 128 CTAs x 4 units in 29.7 us vs 148 CTAs (68 of them with a 4th unit)
   // in 31.7 us; C2 and C4 unchanged (profiles/r02_ab_reuse_balanced_grid.log)
+  // (only when the partial last round is at least a quarter full: with a nearly empty
+  // one, e.g. C2's 896 units = 6 rounds + 8, dropping 20 SMs from every round cost
+  // 8% in a stream of launches, profiles/r02_ab_reuse_balanced_grid.log)
   const int rounds = (plan.total_units + max_ctas - 1) / max_ctas;
   if (rounds <= 0) return 0;
+  const int tail = plan.total_units - (rounds - 1) * max_ctas;
+  if (rounds > 1 && 4 * tail < max_ctas) return max_ctas;
   return (plan.total_units + rounds - 1) / rounds;
 }
 
