@@ -204,6 +204,24 @@ def _check_reuse(batch, got, idx_list, requests=None):
         assert_close(got[c0:c1], ref, f"{wl.name} reuse req {b}")
 
 
+# D = 16 / 32 / 64 run the tcgen05 kernels on their 64-dim layout (round 2): batches large
+# enough for several rounds of the Reuse grid (512 units: 128 CTAs x 4, the balanced
+# grid) and many Refresh units per CTA, every request checked against the oracle
+@pytest.mark.parametrize("D,H,Hk", [(64, 32, 32), (32, 16, 4), (16, 8, 8)])
+def test_narrow_head_dims_multiround(L, D, H, Hk):
+    nreq = 512 // H
+    Ls = [384 + 64 * (b % 5) for b in range(nreq)]
+    bs = [Lb - 32 * (1 + b % 3) for b, Lb in enumerate(Ls)]
+    wl = custom(f"e_d{D}_multi", Ls, bs, [x + 32 for x in bs], H=H, Hk=Hk, D=D, P=64)
+    batch = synth.make_batch(wl)
+    p, out, sc = _run_refresh(L, batch)
+    _check_refresh(batch, out, sc, requests=range(0, nreq, 3))
+    k = oracle_keep_counts(wl)
+    idx = synth.indices(wl, k, mode="random")
+    got = _run_reuse(L, batch, p, join_idx(idx))
+    _check_reuse(batch, got, idx)
+
+
 @pytest.mark.parametrize("mode", ["random", "shared"])
 @pytest.mark.parametrize("cfg,n", [("C0", None), ("C1", 4), ("C2", 4), ("C3", 6)])
 def test_reuse_parity_generated_indices(L, cfg, n, mode):
