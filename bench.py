@@ -733,7 +733,12 @@ def main():
                     "peak": tf_peak, "unit": "TFLOP/s", "frac": kr["frac"],
                     "traffic": ncu_traffic("refresh", args.config),
                     "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
-                    "frac_of_sustained": (kr["TFLOP/s"] / tf_sust) if tf_sust else None}
+                    "frac_of_sustained": (kr["TFLOP/s"] / tf_sust) if tf_sust else None,
+                    "traffic_note": "ncu DRAM bytes per launch (profiles/ncu_traffic.json); the algorithmic bytes "
+                                    "(Q + K + V + O once, + scores) are ~0.54 GB at C1: the LPT unit order "
+                                    "(importance pairs first) reads each (request, KV head)'s K/V a second time "
+                                    "(request-major order: 518 MB, 1.5-2% slower); DRAM ~35% of peak in this "
+                                    "tensor-bound kernel (DESIGN.md §6)"}
         n_launch = 2 if st.mixed else sum(((2 if pc["refresh"] else 0) + (1 if pc["reuse"] else 0)) *
                                           ((pc["wl"].num_requests + 255) // 256) for pc in st.pieces)
         line = {
